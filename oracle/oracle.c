@@ -1,0 +1,184 @@
+/*
+ * oracle.c -- CPU ORACLE FOR THE tm_sgemm HOT PATH.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load or execute this file.  The product library
+ * (paper_1804_10694_b200/, include/tm.h) never links, includes or calls it, and
+ * this file includes nothing from the product: the two share no code.
+ *
+ * What it computes (SI "Introduction"):
+ *
+ *     C = alpha * A * B + beta * C
+ *
+ * written out as its plain definition, in fp64, no blocking, no fusion, no
+ * reordering beyond the definition:
+ *
+ *     R[i,j] = alpha * sum_{p=0}^{k-1} A[i,p] * B[p,j]  +  beta * C0[i,j]
+ *     D[i,j] = |alpha| * sum_{p=0}^{k-1} |A[i,p]| * |B[p,j]|  +  |beta| * |C0[i,j]|
+ *
+ * D is the denominator of the acceptance metric of BASELINE.json north_star:
+ *     err[i,j] = |C_gpu[i,j] - R[i,j]| / D[i,j]  <= 1e-5.
+ *
+ * Readings of points the paper leaves open:
+ *   - storage is row-major, no transposes (reading 1, 2):
+ *       A[i*lda+p], B[p*ldb+j], C0[i*ldc+j];
+ *   - special cases follow reference-BLAS semantics (reading 5):
+ *       beta == 0          -> C0 is NOT read (NaN in C0 does not propagate);
+ *       alpha == 0 or k==0 -> A and B are NOT read, R = beta*C0;
+ *       m == 0 or n == 0   -> nothing is computed.
+ *
+ * Arithmetic: every product of two fp32 values is exact in fp64 (24+24 < 53
+ * significand bits); the sum over p runs in the order p = 0..k-1 for every
+ * (i,j), i.e. the textbook i-j-p loop's order.  The i-p-j loop order below
+ * (a row accumulator acc[0..n)) performs, for each element, exactly the same
+ * fp64 operations in the same order, so it is bit-identical to the i-j-p loop;
+ * it is used only because it reads B row-wise.  OpenMP parallelises over rows
+ * i, which are independent: results do not depend on the thread count.
+ *
+ * Errors: returns 0 on success, -1 on invalid arguments (negative sizes,
+ * leading dimensions smaller than the row length, NULL pointers that would be
+ * read), -2 if the row accumulator cannot be allocated.  Outputs are not
+ * touched on error.
+ *
+ * Pins: tests/test_oracle.py checks this file against exact rational
+ * arithmetic (brute force, all m,n,k in [1,6]), numpy's float64 matmul,
+ * closed forms (identity, permutation, all-ones, alpha=0, beta=0 with NaN
+ * poison), integer-valued inputs, and a hand-computed golden example
+ * (tests/golden/).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static int check_args(int64_t m, int64_t n, int64_t k, float alpha,
+                      const float *A, int64_t lda, const float *B, int64_t ldb,
+                      float beta, const float *C0, int64_t ldc) {
+    if (m < 0 || n < 0 || k < 0) return -1;
+    int reads_ab = (alpha != 0.0f) && (k > 0);
+    if (reads_ab) {
+        if (!A || !B) return -1;
+        if (lda < (k > 1 ? k : 1)) return -1;
+        if (ldb < (n > 1 ? n : 1)) return -1;
+    }
+    if (beta != 0.0f) {
+        if (!C0) return -1;
+        if (ldc < (n > 1 ? n : 1)) return -1;
+    }
+    return 0;
+}
+
+/* One output row i of the definition above, into R_row[0..n), D_row[0..n).
+ * acc/acc_abs are caller-provided scratch of n doubles each. */
+static void oracle_row(int64_t i, int64_t n, int64_t k, float alpha,
+                       const float *A, int64_t lda, const float *B, int64_t ldb,
+                       float beta, const float *C0, int64_t ldc,
+                       double *R_row, double *D_row, double *acc, double *acc_abs) {
+    const double a_alpha = (double)alpha;
+    const double a_beta = (double)beta;
+    for (int64_t j = 0; j < n; ++j) { acc[j] = 0.0; acc_abs[j] = 0.0; }
+    if (alpha != 0.0f) {
+        for (int64_t p = 0; p < k; ++p) {
+            const double a = (double)A[i * lda + p];
+            const double a_abs = fabs(a);
+            const float *Bp = B + p * ldb;
+            for (int64_t j = 0; j < n; ++j) {
+                const double b = (double)Bp[j];
+                acc[j] += a * b;             /* exact product, fp64 sum, p ascending */
+                acc_abs[j] += a_abs * fabs(b);
+            }
+        }
+    }
+    for (int64_t j = 0; j < n; ++j) {
+        double r = 0.0, d = 0.0;
+        if (alpha != 0.0f) {
+            r = a_alpha * acc[j];
+            d = fabs(a_alpha) * acc_abs[j];
+        }
+        if (beta != 0.0f) {               /* beta == 0: C0 is not read */
+            const double c = (double)C0[i * ldc + j];
+            r += a_beta * c;
+            d += fabs(a_beta) * fabs(c);
+        }
+        R_row[j] = r;
+        D_row[j] = d;
+    }
+}
+
+/* Rows rows[0..nrows) of R and D (row t of the outputs is row rows[t] of C);
+ * rows == NULL means all rows 0..m-1 (nrows must then equal m).
+ * R, D are nrows x n, row-major with leading dimension ldr >= n. */
+int tm_oracle_sgemm_rows(int64_t m, int64_t n, int64_t k, float alpha,
+                         const float *A, int64_t lda, const float *B, int64_t ldb,
+                         float beta, const float *C0, int64_t ldc,
+                         int64_t nrows, const int64_t *rows,
+                         double *R, double *D, int64_t ldr) {
+    if (check_args(m, n, k, alpha, A, lda, B, ldb, beta, C0, ldc)) return -1;
+    if (nrows < 0 || ldr < n || (nrows > 0 && (!R || !D))) return -1;
+    if (!rows && nrows != m) return -1;
+    if (rows)
+        for (int64_t t = 0; t < nrows; ++t)
+            if (rows[t] < 0 || rows[t] >= m) return -1;
+    if (nrows == 0 || n == 0) return 0;
+    if (k == 0) alpha = 0.0f;             /* empty sum: A and B are not read */
+    int failed = 0;
+#pragma omp parallel
+    {
+        double *acc = (double *)malloc(sizeof(double) * (size_t)n);
+        double *acc_abs = (double *)malloc(sizeof(double) * (size_t)n);
+        if (!acc || !acc_abs) {
+#pragma omp atomic write
+            failed = 1;
+        } else {
+#pragma omp for schedule(static)
+            for (int64_t t = 0; t < nrows; ++t) {
+                const int64_t i = rows ? rows[t] : t;
+                oracle_row(i, n, k, alpha, A, lda, B, ldb, beta, C0, ldc,
+                           R + t * ldr, D + t * ldr, acc, acc_abs);
+            }
+        }
+        free(acc);
+        free(acc_abs);
+    }
+    return failed ? -2 : 0;
+}
+
+/* All rows: R, D are m x n with leading dimension ldr. */
+int tm_oracle_sgemm_f64(int64_t m, int64_t n, int64_t k, float alpha,
+                        const float *A, int64_t lda, const float *B, int64_t ldb,
+                        float beta, const float *C0, int64_t ldc,
+                        double *R, double *D, int64_t ldr) {
+    return tm_oracle_sgemm_rows(m, n, k, alpha, A, lda, B, ldb, beta, C0, ldc,
+                                m, NULL, R, D, ldr);
+}
+
+/* Row partition of the distributed mode (SURVEY.md 8(b) "Partition rule";
+ * generalises the paper's split(i, N/Ranks), and the rank
+ * conditional q = get_rank(), to P not dividing m):
+ *     rows_r = floor(m/P) + (r < m mod P),  row0_r = r*floor(m/P) + min(r, m mod P). */
+int tm_oracle_dist_rows(int64_t m, int nranks, int rank, int64_t *row0, int64_t *rows) {
+    if (m < 0 || nranks < 1 || rank < 0 || rank >= nranks || !row0 || !rows) return -1;
+    const int64_t q = m / nranks, r = m % nranks;
+    *rows = q + (rank < r ? 1 : 0);
+    *row0 = (int64_t)rank * q + (rank < r ? rank : r);
+    return 0;
+}
+
+void tm_oracle_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
+int tm_oracle_get_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
