@@ -1,0 +1,170 @@
+/*
+ * tm.h -- C ABI of the B200-native fp32 GEMM library (libtm.so).
+ *
+ * The operation (SI "Introduction"): generalized matrix
+ * multiplication
+ *
+ *     C = alpha * A * B + beta * C            (sgemm, fp32)
+ *
+ * in row-major storage with no transposes (reading 1, 2):
+ *
+ *     C[i*ldc + j] = alpha * sum_{p<k} A[i*lda + p] * B[p*ldb + j] + beta * C[i*ldc + j]
+ *     for 0 <= i < m, 0 <= j < n.
+ *
+ * A column-major caller computes the same product by swapping operands:
+ * column-major C(m x n) = A B  <=>  row-major C^T(n x m) = B^T A^T.
+ *
+ * Accuracy contract (BASELINE.json north_star): every element satisfies
+ *     |C - C_ref| / (|alpha| * sum_p |A[i,p]||B[p,j]| + |beta||C0[i,j]|) <= 1e-5
+ * against the exact result C_ref, on every path below.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - All functions are extern "C", never throw, and return tm_status.
+ * - Pointers A, B, C, A_local, ... are DEVICE pointers (cudaMalloc or torch
+ *   allocations on the current device) unless the name says _host.  The caller
+ *   owns every buffer; the library never frees or retains caller memory.
+ *   tm_sgemm / tm_sgemm_ex allocate no device memory.
+ * - stream is a cudaStream_t (passed as void* so this header needs no CUDA
+ *   include); NULL means the legacy default stream.  Calls are stream-ordered
+ *   and return after enqueueing; device faults surface at the caller's next
+ *   synchronisation on that stream.
+ * - Special cases (reference-BLAS semantics, reading 5):
+ *     m == 0 or n == 0        -> no-op, TM_OK;
+ *     alpha == 0 or k == 0    -> A, B are not read, C = beta*C;
+ *     beta == 0               -> C is not read before being written
+ *                                (NaN/Inf already in C do not propagate).
+ * - Invalid arguments (negative sizes, lda < max(1,k), ldb < max(1,n),
+ *   ldc < max(1,n), NULL where a matrix must be read or written, C overlapping
+ *   A or B) return TM_ERR_INVALID_VALUE with C untouched.
+ * - A device other than sm_100 (B200) returns TM_ERR_UNSUPPORTED_DEVICE.
+ *   There is no CPU fallback anywhere in this library.
+ * - Determinism: for fixed inputs, algorithm and device, results are bitwise
+ *   reproducible run to run (no atomics in any reduction).
+ * - Thread safety: calls are reentrant; a tm_comm_t must not be used by two
+ *   host threads at once (NCCL rule).
+ */
+#ifndef TM_H_
+#define TM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TM_OK = 0,
+    TM_ERR_INVALID_VALUE = 1,
+    TM_ERR_UNSUPPORTED_DEVICE = 2,
+    TM_ERR_CUDA = 3,
+    TM_ERR_NCCL = 4,
+    TM_ERR_OUT_OF_MEMORY = 5,
+    TM_ERR_INTERNAL = 6
+} tm_status;
+
+/* Path selection for tm_sgemm_ex.
+ *  TM_ALGO_AUTO      3xTF32 tensor-core path when its layout rules hold
+ *                    (A, B, C 16-byte aligned; lda, ldb, ldc multiples of 4),
+ *                    else the SIMT path.  Misalignment is never an error here.
+ *  TM_ALGO_TF32X3    3xTF32 split-operand tcgen05 MMA (fp32 result, TMEM
+ *                    accumulation).  Misaligned input -> TM_ERR_INVALID_VALUE.
+ *  TM_ALGO_SIMT_F32  pure-FP32 FFMA register-blocked kernel (validation path).
+ *  TM_ALGO_TF32X1    single-pass TF32 (about 1e-3 accuracy; does NOT meet the
+ *                    1e-5 contract; exposed for data-movement bring-up only). */
+typedef enum {
+    TM_ALGO_AUTO = 0,
+    TM_ALGO_TF32X3 = 1,
+    TM_ALGO_SIMT_F32 = 2,
+    TM_ALGO_TF32X1 = 3
+} tm_algo;
+
+/* C = alpha*A*B + beta*C on `stream`.  A: m x k (lda),
+ * B: k x n (ldb), C: m x n (ldc), all row-major fp32 device memory. */
+tm_status tm_sgemm(int64_t m, int64_t n, int64_t k, float alpha,
+                   const float* A, int64_t lda, const float* B, int64_t ldb,
+                   float beta, float* C, int64_t ldc, void* stream);
+
+/* Same operation with an explicit path (tm_algo). */
+tm_status tm_sgemm_ex(int64_t m, int64_t n, int64_t k, float alpha,
+                      const float* A, int64_t lda, const float* B, int64_t ldb,
+                      float beta, float* C, int64_t ldc, void* stream, int algo);
+
+/* End-to-end entry with HOST buffers (ideally pinned): copies A, B (and C when
+ * beta != 0) to the current device, computes, copies C back, and synchronises
+ * `stream` before returning.  Host->device copies of row blocks of A/C overlap
+ * the GEMM of the previous block.  Device staging memory is owned by the
+ * library (grown on demand, cached per device; released by tm_release_workspace).
+ * Errors as above; TM_ERR_OUT_OF_MEMORY if staging cannot be allocated. */
+tm_status tm_sgemm_host(int64_t m, int64_t n, int64_t k, float alpha,
+                        const float* A_host, int64_t lda, const float* B_host, int64_t ldb,
+                        float beta, float* C_host, int64_t ldc, void* stream, int algo);
+
+/* Frees the staging buffers tm_sgemm_host cached on the current device. */
+tm_status tm_release_workspace(void);
+
+/* Human-readable name of a status code (static storage, never NULL). */
+const char* tm_status_string(tm_status s);
+
+/* Library version as major*10000 + minor*100 + patch. */
+int tm_get_version(void);
+
+/* Name of the path tm_sgemm_ex would take for these arguments on the current
+ * device ("tf32x3", "simt", "scale", "noop", or "invalid"); host-only, no launch. */
+const char* tm_sgemm_plan_name(int64_t m, int64_t n, int64_t k, float alpha,
+                               const float* A, int64_t lda, const float* B, int64_t ldb,
+                               float beta, const float* C, int64_t ldc, int algo);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU row-sharded mode (one process per GPU).
+ *
+ * Follows the paper's distribution model: data is distributed across ranks by
+ * rows, each rank computes its own row block
+ * (distribute(i); rank conditional q = get_rank(),
+ * PAPER.md:784-794) and no gather of C is performed.
+ * The only exchange is B: broadcast from `root` (or all-gathered from k-row
+ * shards) with NCCL over NVLink, in K-chunks that overlap the GEMM of the
+ * previous chunk.
+ * ------------------------------------------------------------------------- */
+typedef struct tm_comm_s* tm_comm_t;
+typedef struct { unsigned char bytes[128]; } tm_unique_id; /* wraps ncclUniqueId */
+
+/* Rank 0 creates the id and ships it to all ranks (e.g. torch.distributed). */
+tm_status tm_comm_get_unique_id(tm_unique_id* out);
+
+/* Collective over `nranks` processes; binds to the CURRENT CUDA device.  The
+ * communicator owns one comm stream and its chunk events. */
+tm_status tm_comm_init(tm_comm_t* out, int nranks, int rank, const tm_unique_id* id);
+tm_status tm_comm_destroy(tm_comm_t comm);
+tm_status tm_comm_rank(tm_comm_t comm, int* rank, int* nranks);
+
+/* Balanced block partition of m rows over nranks:
+ *   rows = m/P + (rank < m%P),  row0 = rank*(m/P) + min(rank, m%P). */
+tm_status tm_dist_rows(int64_t m, int nranks, int rank, int64_t* row0, int64_t* rows);
+
+/* Collective: all ranks call with identical m, n, k, alpha, beta, root.
+ *   A_local: rows x k (lda), C_local: rows x n (ldc), rows from tm_dist_rows.
+ *   B: k x n (ldb); valid on `root`; on other ranks a caller-owned k*ldb
+ *      device buffer that is overwritten with root's B.
+ * On return (stream-ordered) C_local = alpha*A_local*B + beta*C_local. */
+tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha,
+                        const float* A_local, int64_t lda, float* B, int64_t ldb, int root,
+                        float beta, float* C_local, int64_t ldc, void* stream);
+
+/* Variant: B is pre-sharded by k-rows (B_shard = rows [k0, k0+kr) of B from
+ * tm_dist_rows(k, ...), leading dimension ldb), all-gathered into the
+ * caller-owned B_full (k x n, ldb).  Requires every rank's shard to have the
+ * same row count (k % nranks == 0), as ncclAllGather does. */
+tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha,
+                                  const float* A_local, int64_t lda, const float* B_shard,
+                                  float* B_full, int64_t ldb, float beta, float* C_local,
+                                  int64_t ldc, void* stream);
+
+/* Bytes this rank received over the communicator since tm_comm_init
+ * (message-conservation accounting used by the tests). */
+tm_status tm_comm_bytes_received(tm_comm_t comm, uint64_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TM_H_ */

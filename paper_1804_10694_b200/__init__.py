@@ -1,0 +1,235 @@
+"""paper_1804_10694_b200 -- B200-native fp32 GEMM (the Tiramisu paper's sgemm).
+
+Thin ctypes binding over the C ABI in ``include/tm.h`` (``_lib/libtm.so``).
+Argument marshalling only: every step of the computation runs in the CUDA
+kernels of the library.  torch is used for device memory, streams and process
+groups.  There is no CPU fallback: if the library is missing this module
+raises at import.
+
+    C = alpha * A @ B + beta * C
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "ALGO_AUTO", "ALGO_TF32X3", "ALGO_SIMT_F32", "ALGO_TF32X1", "TmError", "lib", "lib_path", "sgemm",
+    "sgemm_ex", "sgemm_host", "plan_name", "dist_rows", "Comm", "status_string", "EXPORTED_SYMBOLS",
+]
+
+ALGO_AUTO, ALGO_TF32X3, ALGO_SIMT_F32, ALGO_TF32X1 = 0, 1, 2, 3
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_PKG, "_lib", "libtm.so")
+
+# Every function include/tm.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = [
+    "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
+    "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
+    "tm_dist_rows", "tm_sgemm_dist", "tm_sgemm_dist_allgather", "tm_comm_bytes_received",
+]
+
+
+class TmError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+
+
+def _load():
+    if not os.path.exists(lib_path):
+        raise ImportError(
+            f"{lib_path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(lib_path)
+    i64, f32, vp, ci = ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_int
+    gemm = [i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp]
+    L.tm_sgemm.argtypes = gemm
+    L.tm_sgemm_ex.argtypes = gemm + [ci]
+    L.tm_sgemm_host.argtypes = gemm + [ci]
+    L.tm_sgemm_plan_name.argtypes = [i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, ci]
+    L.tm_sgemm_plan_name.restype = ctypes.c_char_p
+    L.tm_status_string.argtypes = [ci]
+    L.tm_status_string.restype = ctypes.c_char_p
+    L.tm_dist_rows.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.tm_comm_get_unique_id.argtypes = [vp]
+    L.tm_comm_init.argtypes = [ctypes.POINTER(vp), ci, ci, vp]
+    L.tm_comm_destroy.argtypes = [vp]
+    L.tm_comm_rank.argtypes = [vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
+    L.tm_comm_bytes_received.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+    L.tm_sgemm_dist.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, i64, ci, f32, vp, i64, vp]
+    L.tm_sgemm_dist_allgather.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, vp, i64, f32, vp, i64, vp]
+    for name in EXPORTED_SYMBOLS:
+        fn = getattr(L, name)
+        if fn.restype is ctypes.c_int or name in ("tm_status_string", "tm_sgemm_plan_name"):
+            continue
+        fn.restype = ctypes.c_int
+    return L
+
+
+lib = _load()
+
+
+def status_string(status: int) -> str:
+    return lib.tm_status_string(int(status)).decode()
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise TmError(status, what)
+
+
+def _ld(t) -> int:
+    """Leading dimension (elements) of a row-major 2-D view with unit column stride."""
+    if t.dim() != 2:
+        raise ValueError("expected a 2-D tensor")
+    if t.shape[1] > 1 and t.stride(1) != 1:
+        raise ValueError("expected unit column stride (row-major)")
+    if t.shape[0] <= 1:
+        return max(int(t.stride(0)) if t.shape[0] == 1 else 1, int(t.shape[1]), 1)
+    return int(t.stride(0))
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _f32(name, t):
+    import torch
+    if t is None:
+        return None
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32")
+    return t
+
+
+def sgemm_ex(A, B, C, alpha: float = 1.0, beta: float = 0.0, algo: int = ALGO_AUTO, stream=None,
+             m=None, n=None, k=None):
+    """In place: C <- alpha*A@B + beta*C on CUDA tensors (row-major 2-D views).
+
+    A may be None when alpha == 0 or k == 0 (it is then not read), likewise B.
+    """
+    A, B, C = _f32("A", A), _f32("B", B), _f32("C", C)
+    m = C.shape[0] if m is None else m
+    n = C.shape[1] if n is None else n
+    k = (A.shape[1] if A is not None else 0) if k is None else k
+    lda = _ld(A) if A is not None else max(k, 1)
+    ldb = _ld(B) if B is not None else max(n, 1)
+    st = lib.tm_sgemm_ex(m, n, k, float(alpha), _ptr(A), lda, _ptr(B), ldb, float(beta), _ptr(C), _ld(C),
+                         _stream(stream), int(algo))
+    _check(st, "tm_sgemm_ex")
+    return C
+
+
+def sgemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None):
+    """C <- alpha*A@B + beta*C (AUTO path: 3xTF32 tensor cores when aligned)."""
+    return sgemm_ex(A, B, C, alpha, beta, ALGO_AUTO, stream)
+
+
+def plan_name(m, n, k, alpha=1.0, beta=0.0, A_ptr=0, lda=None, B_ptr=0, ldb=None, C_ptr=0, ldc=None,
+              algo=ALGO_AUTO) -> str:
+    """Host-only: the path tm_sgemm_ex would take (no device needed)."""
+    lda = max(k, 1) if lda is None else lda
+    ldb = max(n, 1) if ldb is None else ldb
+    ldc = max(n, 1) if ldc is None else ldc
+    return lib.tm_sgemm_plan_name(m, n, k, float(alpha), ctypes.c_void_p(A_ptr), lda, ctypes.c_void_p(B_ptr),
+                                  ldb, float(beta), ctypes.c_void_p(C_ptr), ldc, int(algo)).decode()
+
+
+def sgemm_host(A, B, C, alpha: float = 1.0, beta: float = 0.0, algo: int = ALGO_AUTO, stream=None):
+    """End-to-end on HOST (CPU, ideally pinned) float32 tensors/arrays: copies in,
+    computes on the current GPU, copies C back; synchronous."""
+    import numpy as np
+
+    def info(x):
+        if x is None:
+            return None, 0
+        if isinstance(x, np.ndarray):
+            if x.dtype != np.float32:
+                raise TypeError("float32 required")
+            ld = x.strides[0] // 4 if x.shape[0] > 1 else max(x.shape[1], 1)
+            return ctypes.c_void_p(x.ctypes.data), ld
+        if x.is_cuda:
+            raise ValueError("sgemm_host takes host buffers")
+        return ctypes.c_void_p(x.data_ptr()), _ld(x)
+
+    pa, lda = info(A)
+    pb, ldb = info(B)
+    pc, ldc = info(C)
+    m, n = C.shape
+    k = A.shape[1] if A is not None else 0
+    st = lib.tm_sgemm_host(m, n, k, float(alpha), pa, lda or max(k, 1), pb, ldb or max(n, 1), float(beta), pc,
+                           ldc, _stream(stream), int(algo))
+    _check(st, "tm_sgemm_host")
+    return C
+
+
+def dist_rows(m: int, nranks: int, rank: int):
+    r0, nr = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.tm_dist_rows(m, nranks, rank, ctypes.byref(r0), ctypes.byref(nr)), "tm_dist_rows")
+    return r0.value, nr.value
+
+
+class Comm:
+    """NCCL communicator owned by libtm (one process per GPU).
+
+    Bootstrap: rank 0 creates the unique id, every rank receives it through the
+    given torch.distributed process group (any backend), then all ranks init.
+    """
+
+    def __init__(self, rank: int, nranks: int, group=None):
+        import torch
+        import torch.distributed as dist
+        uid = (ctypes.c_ubyte * 128)()
+        if rank == 0:
+            _check(lib.tm_comm_get_unique_id(ctypes.byref(uid)), "tm_comm_get_unique_id")
+        if nranks > 1:
+            obj = [bytes(uid) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            ctypes.memmove(uid, obj[0], 128)
+        h = ctypes.c_void_p()
+        _check(lib.tm_comm_init(ctypes.byref(h), nranks, rank, ctypes.byref(uid)), "tm_comm_init")
+        self.handle = h
+        self.rank, self.nranks = rank, nranks
+        self._torch = torch
+
+    def close(self):
+        if self.handle:
+            _check(lib.tm_comm_destroy(self.handle), "tm_comm_destroy")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def bytes_received(self) -> int:
+        v = ctypes.c_uint64()
+        _check(lib.tm_comm_bytes_received(self.handle, ctypes.byref(v)), "tm_comm_bytes_received")
+        return int(v.value)
+
+    def sgemm(self, m, n, k, A_local, B, C_local, alpha=1.0, beta=0.0, root=0, stream=None):
+        """Row-sharded C_local <- alpha*A_local@B + beta*C_local; B broadcast from root."""
+        st = lib.tm_sgemm_dist(self.handle, m, n, k, float(alpha), _ptr(A_local),
+                               _ld(A_local) if A_local is not None and A_local.shape[0] > 0 else max(k, 1),
+                               _ptr(B), _ld(B), int(root), float(beta), _ptr(C_local),
+                               _ld(C_local) if C_local.shape[0] > 0 else max(n, 1), _stream(stream))
+        _check(st, "tm_sgemm_dist")
+        return C_local
+
+    def sgemm_allgather(self, m, n, k, A_local, B_shard, B_full, C_local, alpha=1.0, beta=0.0, stream=None):
+        st = lib.tm_sgemm_dist_allgather(self.handle, m, n, k, float(alpha), _ptr(A_local),
+                                         _ld(A_local) if A_local.shape[0] > 0 else max(k, 1), _ptr(B_shard),
+                                         _ptr(B_full), _ld(B_full), float(beta), _ptr(C_local),
+                                         _ld(C_local) if C_local.shape[0] > 0 else max(n, 1), _stream(stream))
+        _check(st, "tm_sgemm_dist_allgather")
+        return C_local

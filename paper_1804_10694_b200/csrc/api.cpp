@@ -1,0 +1,328 @@
+// api.cpp -- the C ABI (include/tm.h): argument validation, special cases,
+// path selection and the end-to-end host-buffer entry.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "tm_internal.h"
+
+namespace tmk {
+namespace {
+
+constexpr int kMaxDevices = 64;
+
+struct DevInfo {
+  int sms = 0;
+  int major = 0, minor = 0;
+  bool ok = false;
+};
+
+DevInfo g_dev[kMaxDevices];
+std::once_flag g_dev_once[kMaxDevices];
+
+bool log_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TM_LOG");
+    v = (e && e[0] && e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+tm_status current_device(DevInfo** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TM_ERR_CUDA;
+  if (dev < 0 || dev >= kMaxDevices) return TM_ERR_UNSUPPORTED_DEVICE;
+  std::call_once(g_dev_once[dev], [dev]() {
+    DevInfo& d = g_dev[dev];
+    if (cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return;
+    if (cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return;
+    if (cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) return;
+    d.ok = true;
+  });
+  DevInfo& d = g_dev[dev];
+  if (!d.ok) return TM_ERR_CUDA;
+  // This library is compiled for sm_100a only (B200).
+  if (!(d.major == 10 && d.minor == 0)) return TM_ERR_UNSUPPORTED_DEVICE;
+  *out = &d;
+  return TM_OK;
+}
+
+bool ranges_overlap(const void* a, int64_t abytes, const void* b, int64_t bbytes) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  return a0 < b0 + static_cast<uintptr_t>(bbytes) && b0 < a0 + static_cast<uintptr_t>(abytes);
+}
+
+int64_t extent_bytes(int64_t rows, int64_t cols, int64_t ld) {
+  if (rows <= 0 || cols <= 0) return 0;
+  return ((rows - 1) * ld + cols) * 4;
+}
+
+enum class Path { kInvalid, kNoop, kScale, kTc, kSimt };
+
+struct Plan {
+  Path path = Path::kInvalid;
+  TcChoice tc{2, 128, true};
+};
+
+bool tc_aligned(const GemmArgs& a) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  return al16(a.A) && al16(a.B) && al16(a.C) && (a.lda % 4 == 0) && (a.ldb % 4 == 0) && (a.ldc % 4 == 0);
+}
+
+// Host-only validation + path choice (no CUDA calls).
+Plan make_plan(const GemmArgs& a, int algo, int num_sms) {
+  Plan pl;
+  if (a.m < 0 || a.n < 0 || a.k < 0) return pl;
+  if (algo < TM_ALGO_AUTO || algo > TM_ALGO_TF32X1) return pl;
+  if (a.m == 0 || a.n == 0) {
+    pl.path = Path::kNoop;
+    return pl;
+  }
+  const int64_t nn = a.n > 1 ? a.n : 1, kk = a.k > 1 ? a.k : 1;
+  if (!a.C || a.ldc < nn) return pl;
+  const bool reads_ab = (a.alpha != 0.0f) && (a.k > 0);
+  if (!reads_ab) {
+    pl.path = Path::kScale;
+    return pl;
+  }
+  if (!a.A || !a.B || a.lda < kk || a.ldb < nn) return pl;
+  const int64_t cbytes = extent_bytes(a.m, a.n, a.ldc);
+  if (ranges_overlap(a.C, cbytes, a.A, extent_bytes(a.m, a.k, a.lda)) ||
+      ranges_overlap(a.C, cbytes, a.B, extent_bytes(a.k, a.n, a.ldb)))
+    return pl;
+  const bool aligned = tc_aligned(a);
+  switch (algo) {
+    case TM_ALGO_SIMT_F32:
+      pl.path = Path::kSimt;
+      break;
+    case TM_ALGO_TF32X3:
+    case TM_ALGO_TF32X1:
+      if (!aligned) return pl;
+      pl.path = Path::kTc;
+      break;
+    default:
+      pl.path = aligned ? Path::kTc : Path::kSimt;
+  }
+  if (pl.path == Path::kTc) {
+    pl.tc = plan_tc(a.m, a.n, a.k, num_sms > 0 ? num_sms : 148);
+    pl.tc.split3 = (algo != TM_ALGO_TF32X1);
+    const char* force = std::getenv("TM_TC_CONFIG");  // "cg,bn" -- tests/bench only
+    if (force) {
+      int cg = 0, bn = 0;
+      if (std::sscanf(force, "%d,%d", &cg, &bn) == 2 && (cg == 1 || cg == 2) && (bn == 32 || bn == 64 || bn == 128)) {
+        pl.tc.cg = cg;
+        pl.tc.bn_cta = bn;
+      }
+    }
+  }
+  return pl;
+}
+
+tm_status run(const GemmArgs& a, int algo, cudaStream_t stream) {
+  // Host-side validation first: invalid arguments never touch the device.
+  Plan pre = make_plan(a, algo, 148);
+  if (pre.path == Path::kInvalid) return TM_ERR_INVALID_VALUE;
+  if (pre.path == Path::kNoop) return TM_OK;
+  DevInfo* dev = nullptr;
+  tm_status st = current_device(&dev);
+  if (st != TM_OK) return st;
+  Plan pl = make_plan(a, algo, dev->sms);
+  if (log_enabled())
+    std::fprintf(stderr, "[tm] sgemm m=%lld n=%lld k=%lld algo=%d -> %s cg=%d bn=%d split3=%d\n",
+                 static_cast<long long>(a.m), static_cast<long long>(a.n), static_cast<long long>(a.k), algo,
+                 pl.path == Path::kTc ? "tf32x3" : pl.path == Path::kSimt ? "simt" : "scale", pl.tc.cg,
+                 pl.tc.bn_cta, pl.tc.split3 ? 1 : 0);
+  switch (pl.path) {
+    case Path::kScale:
+      return launch_scale(a.m, a.n, a.beta, a.C, a.ldc, stream);
+    case Path::kSimt:
+      return launch_simt(a, stream);
+    case Path::kTc:
+      return launch_tc(a, pl.tc, dev->sms, stream);
+    default:
+      return TM_ERR_INTERNAL;
+  }
+}
+
+// ------------------------------------------------------------ host e2e staging
+struct Workspace {
+  float* buf = nullptr;
+  size_t bytes = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  static constexpr int kEv = 16;
+  cudaEvent_t ev_in[kEv] = {}, ev_out[kEv] = {};
+  bool init = false;
+};
+Workspace g_ws[kMaxDevices];
+std::mutex g_ws_mu;
+
+tm_status ws_get(int dev, size_t bytes, Workspace** out) {
+  Workspace& w = g_ws[dev];
+  if (!w.init) {
+    if (cudaStreamCreateWithFlags(&w.h2d, cudaStreamNonBlocking) != cudaSuccess) return TM_ERR_CUDA;
+    if (cudaStreamCreateWithFlags(&w.d2h, cudaStreamNonBlocking) != cudaSuccess) return TM_ERR_CUDA;
+    for (int i = 0; i < Workspace::kEv; ++i) {
+      if (cudaEventCreateWithFlags(&w.ev_in[i], cudaEventDisableTiming) != cudaSuccess) return TM_ERR_CUDA;
+      if (cudaEventCreateWithFlags(&w.ev_out[i], cudaEventDisableTiming) != cudaSuccess) return TM_ERR_CUDA;
+    }
+    w.init = true;
+  }
+  if (w.bytes < bytes) {
+    if (w.buf) cudaFree(w.buf);
+    w.buf = nullptr;
+    w.bytes = 0;
+    if (cudaMalloc(&w.buf, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return TM_ERR_OUT_OF_MEMORY;
+    }
+    w.bytes = bytes;
+  }
+  *out = &w;
+  return TM_OK;
+}
+
+}  // namespace
+}  // namespace tmk
+
+using tmk::GemmArgs;
+
+extern "C" {
+
+tm_status tm_sgemm_ex(int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda, const float* B,
+                      int64_t ldb, float beta, float* C, int64_t ldc, void* stream, int algo) {
+  GemmArgs a{m, n, k, alpha, beta, A, lda, B, ldb, C, ldc};
+  try {
+    return tmk::run(a, algo, static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return TM_ERR_INTERNAL;
+  }
+}
+
+tm_status tm_sgemm(int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda, const float* B,
+                   int64_t ldb, float beta, float* C, int64_t ldc, void* stream) {
+  return tm_sgemm_ex(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, stream, TM_ALGO_AUTO);
+}
+
+const char* tm_sgemm_plan_name(int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda,
+                               const float* B, int64_t ldb, float beta, const float* C, int64_t ldc, int algo) {
+  GemmArgs a{m, n, k, alpha, beta, A, lda, B, ldb, const_cast<float*>(C), ldc};
+  tmk::Plan pl = tmk::make_plan(a, algo, 148);
+  switch (pl.path) {
+    case tmk::Path::kNoop: return "noop";
+    case tmk::Path::kScale: return "scale";
+    case tmk::Path::kSimt: return "simt";
+    case tmk::Path::kTc: return pl.tc.split3 ? "tf32x3" : "tf32x1";
+    default: return "invalid";
+  }
+}
+
+const char* tm_status_string(tm_status s) {
+  switch (s) {
+    case TM_OK: return "TM_OK";
+    case TM_ERR_INVALID_VALUE: return "TM_ERR_INVALID_VALUE";
+    case TM_ERR_UNSUPPORTED_DEVICE: return "TM_ERR_UNSUPPORTED_DEVICE";
+    case TM_ERR_CUDA: return "TM_ERR_CUDA";
+    case TM_ERR_NCCL: return "TM_ERR_NCCL";
+    case TM_ERR_OUT_OF_MEMORY: return "TM_ERR_OUT_OF_MEMORY";
+    case TM_ERR_INTERNAL: return "TM_ERR_INTERNAL";
+  }
+  return "TM_ERR_UNKNOWN";
+}
+
+int tm_get_version(void) { return 100; }  // 0.1.0
+
+// End-to-end with host buffers.  Row blocks of A and C stream in on the h2d
+// stream while earlier blocks compute on `stream`; results stream back on the
+// d2h stream (PCIe is full duplex).  Rows are independent, so the row-block
+// schedule does not change which products enter each element's sum.
+tm_status tm_sgemm_host(int64_t m, int64_t n, int64_t k, float alpha, const float* A_host, int64_t lda,
+                        const float* B_host, int64_t ldb, float beta, float* C_host, int64_t ldc, void* stream_,
+                        int algo) {
+  try {
+    GemmArgs chk{m, n, k, alpha, beta, A_host, lda, B_host, ldb, C_host, ldc};
+    tmk::Plan pre = tmk::make_plan(chk, algo == TM_ALGO_TF32X3 || algo == TM_ALGO_TF32X1 ? TM_ALGO_SIMT_F32 : algo, 148);
+    if (pre.path == tmk::Path::kInvalid) return TM_ERR_INVALID_VALUE;
+    if (pre.path == tmk::Path::kNoop) return TM_OK;
+    tmk::DevInfo* dev = nullptr;
+    tm_status st = tmk::current_device(&dev);
+    if (st != TM_OK) return st;
+    int devid = 0;
+    cudaGetDevice(&devid);
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    const bool reads_ab = (alpha != 0.0f) && (k > 0);
+    const bool reads_c = (beta != 0.0f);
+    // Device copies are dense with 16-B aligned pitch (multiple of 4 floats).
+    auto pad4 = [](int64_t x) { return (x + 3) / 4 * 4; };
+    const int64_t dlda = pad4(k > 0 ? k : 1), dldb = pad4(n), dldc = pad4(n);
+    const size_t a_el = reads_ab ? static_cast<size_t>(m) * dlda : 0;
+    const size_t b_el = reads_ab ? static_cast<size_t>(k) * dldb : 0;
+    const size_t c_el = static_cast<size_t>(m) * dldc;
+    std::lock_guard<std::mutex> lk(tmk::g_ws_mu);
+    tmk::Workspace* w = nullptr;
+    st = tmk::ws_get(devid, (a_el + b_el + c_el) * 4 + 256, &w);
+    if (st != TM_OK) return st;
+    float* dA = w->buf;
+    float* dB = dA + a_el;
+    float* dC = dB + b_el;
+    // Row blocks: up to 8, at least 256 rows each.
+    int nblk = static_cast<int>((m + 255) / 256);
+    if (nblk > 8) nblk = 8;
+    if (nblk < 1) nblk = 1;
+    const int64_t rows_per = (m + nblk - 1) / nblk;
+    cudaEvent_t start_ev = w->ev_out[tmk::Workspace::kEv - 1];
+    if (cudaEventRecord(start_ev, stream) != cudaSuccess) return TM_ERR_CUDA;
+    if (cudaStreamWaitEvent(w->h2d, start_ev, 0) != cudaSuccess) return TM_ERR_CUDA;
+    if (reads_ab) {
+      if (cudaMemcpy2DAsync(dB, dldb * 4, B_host, ldb * 4, n * 4, k, cudaMemcpyHostToDevice, w->h2d) != cudaSuccess)
+        return TM_ERR_CUDA;
+    }
+    for (int b = 0; b < nblk; ++b) {
+      const int64_t r0 = b * rows_per;
+      const int64_t rows = (r0 + rows_per <= m) ? rows_per : m - r0;
+      if (rows <= 0) break;
+      if (reads_ab && k > 0) {
+        if (cudaMemcpy2DAsync(dA + r0 * dlda, dlda * 4, A_host + r0 * lda, lda * 4, k * 4, rows,
+                              cudaMemcpyHostToDevice, w->h2d) != cudaSuccess)
+          return TM_ERR_CUDA;
+      }
+      if (reads_c) {
+        if (cudaMemcpy2DAsync(dC + r0 * dldc, dldc * 4, C_host + r0 * ldc, ldc * 4, n * 4, rows,
+                              cudaMemcpyHostToDevice, w->h2d) != cudaSuccess)
+          return TM_ERR_CUDA;
+      }
+      if (cudaEventRecord(w->ev_in[b], w->h2d) != cudaSuccess) return TM_ERR_CUDA;
+      if (cudaStreamWaitEvent(stream, w->ev_in[b], 0) != cudaSuccess) return TM_ERR_CUDA;
+      GemmArgs a{rows, n, k, alpha, beta, dA + r0 * dlda, dlda, dB, dldb, dC + r0 * dldc, dldc};
+      st = tmk::run(a, algo, stream);
+      if (st != TM_OK) return st;
+      if (cudaEventRecord(w->ev_out[b], stream) != cudaSuccess) return TM_ERR_CUDA;
+      if (cudaStreamWaitEvent(w->d2h, w->ev_out[b], 0) != cudaSuccess) return TM_ERR_CUDA;
+      if (cudaMemcpy2DAsync(C_host + r0 * ldc, ldc * 4, dC + r0 * dldc, dldc * 4, n * 4, rows,
+                            cudaMemcpyDeviceToHost, w->d2h) != cudaSuccess)
+        return TM_ERR_CUDA;
+    }
+    if (cudaStreamSynchronize(w->d2h) != cudaSuccess) return TM_ERR_CUDA;
+    if (cudaStreamSynchronize(stream) != cudaSuccess) return TM_ERR_CUDA;
+    return TM_OK;
+  } catch (...) {
+    return TM_ERR_INTERNAL;
+  }
+}
+
+tm_status tm_release_workspace(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TM_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(tmk::g_ws_mu);
+  tmk::Workspace& w = tmk::g_ws[dev];
+  if (w.buf) cudaFree(w.buf);
+  w.buf = nullptr;
+  w.bytes = 0;
+  return TM_OK;
+}
+
+}  // extern "C"

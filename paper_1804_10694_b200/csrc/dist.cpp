@@ -1,0 +1,236 @@
+// dist.cpp -- row-sharded multi-GPU sgemm (one process per GPU).
+//
+// The paper's distributed model: data distributed by rows,
+// each rank runs its own block (distribute(i); rank conditional
+// q = get_rank()), communication is explicit
+// (send/receive) and C is never gathered.
+// For gemm the only exchange is B: NCCL broadcast from the root over
+// NVLink/NVSwitch, in K-chunks on a dedicated comm stream; the GEMM of chunk c
+// (beta_c = beta for c = 0, else 1) runs on the caller's stream as soon as
+// chunk c has arrived, so chunk c+1 streams while chunk c computes.
+//
+// NCCL is loaded with dlopen (the same libnccl.so.2 torch uses), so the
+// single-GPU library has no link-time NCCL dependency.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "tm_internal.h"
+
+namespace {
+
+// Minimal NCCL ABI (stable since NCCL 2.x; matches nccl.h).
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef enum { ncclSuccess = 0 } ncclResult_t;
+typedef enum { ncclFloat32 = 7 } ncclDataType_t;
+
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  bool ok = false;
+};
+
+Nccl g_nccl;
+std::once_flag g_nccl_once;
+
+void load_nccl() {
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    const char* p = std::getenv("TM_NCCL_PATH");
+    if (p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+  }
+  if (!h) return;
+  g_nccl.GetUniqueId = reinterpret_cast<decltype(g_nccl.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+  g_nccl.CommInitRank = reinterpret_cast<decltype(g_nccl.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+  g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+  g_nccl.Broadcast = reinterpret_cast<decltype(g_nccl.Broadcast)>(dlsym(h, "ncclBroadcast"));
+  g_nccl.AllGather = reinterpret_cast<decltype(g_nccl.AllGather)>(dlsym(h, "ncclAllGather"));
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.Broadcast && g_nccl.AllGather;
+}
+
+bool nccl() {
+  std::call_once(g_nccl_once, load_nccl);
+  return g_nccl.ok;
+}
+
+constexpr int kMaxChunks = 16;
+
+}  // namespace
+
+struct tm_comm_s {
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1, device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_chunk[kMaxChunks] = {};
+  uint64_t bytes_received = 0;
+};
+
+extern "C" {
+
+tm_status tm_dist_rows(int64_t m, int nranks, int rank, int64_t* row0, int64_t* rows) {
+  if (m < 0 || nranks < 1 || rank < 0 || rank >= nranks || !row0 || !rows) return TM_ERR_INVALID_VALUE;
+  const int64_t q = m / nranks, r = m % nranks;
+  *rows = q + (rank < r ? 1 : 0);
+  *row0 = static_cast<int64_t>(rank) * q + (rank < r ? rank : r);
+  return TM_OK;
+}
+
+tm_status tm_comm_get_unique_id(tm_unique_id* out) {
+  if (!out) return TM_ERR_INVALID_VALUE;
+  if (!nccl()) return TM_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == sizeof(tm_unique_id), "unique id size");
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return TM_ERR_NCCL;
+  std::memcpy(out->bytes, id.internal, sizeof(id));
+  return TM_OK;
+}
+
+tm_status tm_comm_init(tm_comm_t* out, int nranks, int rank, const tm_unique_id* id) {
+  if (!out || !id || nranks < 1 || rank < 0 || rank >= nranks) return TM_ERR_INVALID_VALUE;
+  if (!nccl()) return TM_ERR_NCCL;
+  tm_comm_s* c = new (std::nothrow) tm_comm_s;
+  if (!c) return TM_ERR_OUT_OF_MEMORY;
+  c->rank = rank;
+  c->nranks = nranks;
+  if (cudaGetDevice(&c->device) != cudaSuccess) { delete c; return TM_ERR_CUDA; }
+  ncclUniqueId nid;
+  std::memcpy(nid.internal, id->bytes, sizeof(nid));
+  if (g_nccl.CommInitRank(&c->comm, nranks, nid, rank) != ncclSuccess) { delete c; return TM_ERR_NCCL; }
+  bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) == cudaSuccess;
+  for (int i = 0; ok && i < kMaxChunks; ++i)
+    ok = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    tm_comm_destroy(c);
+    return TM_ERR_CUDA;
+  }
+  *out = c;
+  return TM_OK;
+}
+
+tm_status tm_comm_destroy(tm_comm_t c) {
+  if (!c) return TM_ERR_INVALID_VALUE;
+  tm_status st = TM_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm && g_nccl.CommDestroy(c->comm) != ncclSuccess) st = TM_ERR_NCCL;
+  for (int i = 0; i < kMaxChunks; ++i)
+    if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return st;
+}
+
+tm_status tm_comm_rank(tm_comm_t c, int* rank, int* nranks) {
+  if (!c || !rank || !nranks) return TM_ERR_INVALID_VALUE;
+  *rank = c->rank;
+  *nranks = c->nranks;
+  return TM_OK;
+}
+
+tm_status tm_comm_bytes_received(tm_comm_t c, uint64_t* bytes) {
+  if (!c || !bytes) return TM_ERR_INVALID_VALUE;
+  *bytes = c->bytes_received;
+  return TM_OK;
+}
+
+static int choose_chunks(int64_t k, int nranks) {
+  if (nranks <= 1) return 1;
+  // Chunks of at least 512 K-rows; at most 8 (the first chunk is the exposed
+  // transfer, later ones hide behind the previous chunk's GEMM).
+  int64_t c = k / 512;
+  if (c > 8) c = 8;
+  if (c < 1) c = 1;
+  return static_cast<int>(c);
+}
+
+tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha, const float* A_local,
+                        int64_t lda, float* B, int64_t ldb, int root, float beta, float* C_local, int64_t ldc,
+                        void* stream_) {
+  if (!comm || root < 0 || root >= comm->nranks || m < 0 || n < 0 || k < 0) return TM_ERR_INVALID_VALUE;
+  int64_t row0 = 0, rows = 0;
+  tm_dist_rows(m, comm->nranks, comm->rank, &row0, &rows);
+  (void)row0;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const bool reads_ab = alpha != 0.0f && k > 0 && n > 0;
+  if (!reads_ab || comm->nranks == 1) {
+    // Nothing to exchange (P == 1, or B is not read): exactly tm_sgemm.
+    return tm_sgemm(rows, n, k, alpha, A_local, lda, B, ldb, beta, C_local, ldc, stream);
+  }
+  if (!B || ldb < (n > 1 ? n : 1)) return TM_ERR_INVALID_VALUE;
+  const int nch = choose_chunks(k, comm->nranks);
+  const int64_t kc = ((k + nch - 1) / nch + 31) / 32 * 32;
+  if (cudaEventRecord(comm->ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (cudaStreamWaitEvent(comm->stream, comm->ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
+  int used = 0;
+  for (int64_t k0 = 0; k0 < k; k0 += kc, ++used) {
+    const int64_t kr = (k0 + kc <= k) ? kc : k - k0;
+    // Root sends in place; the last row's padding beyond n is inside k*ldb.
+    const size_t count = static_cast<size_t>(kr) * static_cast<size_t>(ldb);
+    float* p = B + k0 * ldb;
+    if (g_nccl.Broadcast(p, p, count, ncclFloat32, root, comm->comm, comm->stream) != ncclSuccess)
+      return TM_ERR_NCCL;
+    if (comm->rank != root) comm->bytes_received += count * 4;
+    if (cudaEventRecord(comm->ev_chunk[used], comm->stream) != cudaSuccess) return TM_ERR_CUDA;
+  }
+  used = 0;
+  for (int64_t k0 = 0; k0 < k; k0 += kc, ++used) {
+    const int64_t kr = (k0 + kc <= k) ? kc : k - k0;
+    if (cudaStreamWaitEvent(stream, comm->ev_chunk[used], 0) != cudaSuccess) return TM_ERR_CUDA;
+    if (rows > 0) {
+      tm_status st = tm_sgemm(rows, n, kr, alpha, A_local + k0, lda, B + k0 * ldb, ldb, k0 == 0 ? beta : 1.0f,
+                              C_local, ldc, stream);
+      if (st != TM_OK) return st;
+    }
+  }
+  return TM_OK;
+}
+
+tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha,
+                                  const float* A_local, int64_t lda, const float* B_shard, float* B_full,
+                                  int64_t ldb, float beta, float* C_local, int64_t ldc, void* stream_) {
+  if (!comm || m < 0 || n < 0 || k < 0) return TM_ERR_INVALID_VALUE;
+  if (k % comm->nranks != 0) return TM_ERR_INVALID_VALUE;
+  int64_t row0 = 0, rows = 0;
+  tm_dist_rows(m, comm->nranks, comm->rank, &row0, &rows);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const bool reads_ab = alpha != 0.0f && k > 0 && n > 0;
+  if (!reads_ab) return tm_sgemm(rows, n, k, alpha, A_local, lda, B_full, ldb, beta, C_local, ldc, stream);
+  if (!B_shard || !B_full || ldb < (n > 1 ? n : 1)) return TM_ERR_INVALID_VALUE;
+  const int64_t kr = k / comm->nranks, k0 = comm->rank * kr;
+  if (cudaEventRecord(comm->ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (cudaStreamWaitEvent(comm->stream, comm->ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
+  const size_t count = static_cast<size_t>(kr) * static_cast<size_t>(ldb);
+  if (g_nccl.AllGather(B_shard, B_full, count, ncclFloat32, comm->comm, comm->stream) != ncclSuccess)
+    return TM_ERR_NCCL;
+  comm->bytes_received += count * 4 * static_cast<uint64_t>(comm->nranks - 1);
+  if (cudaEventRecord(comm->ev_chunk[0], comm->stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (rows == 0) return cudaStreamWaitEvent(stream, comm->ev_chunk[0], 0) == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+  // Own shard first: it is already resident, so it overlaps the all-gather.
+  tm_status st = tm_sgemm(rows, n, kr, alpha, A_local + k0, lda, B_shard, ldb, beta, C_local, ldc, stream);
+  if (st != TM_OK) return st;
+  if (cudaStreamWaitEvent(stream, comm->ev_chunk[0], 0) != cudaSuccess) return TM_ERR_CUDA;
+  if (k0 > 0) {
+    st = tm_sgemm(rows, n, k0, alpha, A_local, lda, B_full, ldb, 1.0f, C_local, ldc, stream);
+    if (st != TM_OK) return st;
+  }
+  if (k0 + kr < k) {
+    st = tm_sgemm(rows, n, k - k0 - kr, alpha, A_local + k0 + kr, lda, B_full + (k0 + kr) * ldb, ldb, 1.0f,
+                  C_local, ldc, stream);
+    if (st != TM_OK) return st;
+  }
+  return TM_OK;
+}
+
+}  // extern "C"

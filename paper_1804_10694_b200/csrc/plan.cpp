@@ -1,0 +1,43 @@
+// plan.cpp -- tile-configuration planner for the tensor-core path.
+//
+// The paper auto-tunes tile sizes for its sgemm; here the
+// choice is a closed-form cost model over the compiled configurations:
+// makespan = waves x per-tile MMA time / efficiency, where
+//   tile      = (128*cg) x (bn*cg)            (CTA pair when cg == 2)
+//   waves     = ceil(tiles / (num_sms / cg))  (persistent clusters)
+//   per-tile  = ceil(k/32) * 4 K=8 steps * 3 MMAs * (cg*bn/2) cycles
+//               (tcgen05 floor max(M,128)*N/(256*cg) with M = 128*cg, N = bn*cg)
+//   efficiency: 1-CTA tiles read both operands from one SM's shared memory
+//               (about 1.5x the smem bytes per MMA of a CTA pair), and narrow
+//               tiles pay fixed per-stage costs -- measured factors, DESIGN.md.
+#include <cstdint>
+
+#include "tm_internal.h"
+
+namespace tmk {
+
+TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms) {
+  static const TcChoice cands[] = {{2, 128, true}, {2, 64, true}, {2, 32, true},
+                                   {1, 128, true}, {1, 64, true}, {1, 32, true}};
+  TcChoice best = cands[0];
+  double best_t = 1e300;
+  const int64_t kb = (k + 31) / 32;
+  for (const TcChoice& c : cands) {
+    const int64_t tile_m = 128LL * c.cg, tile_n = static_cast<int64_t>(c.bn_cta) * c.cg;
+    const int64_t tiles = ((m + tile_m - 1) / tile_m) * ((n + tile_n - 1) / tile_n);
+    const int64_t units = num_sms / c.cg;
+    const int64_t waves = (tiles + units - 1) / units;
+    double per_tile = static_cast<double>(kb) * 4.0 * 3.0 * (c.cg * c.bn_cta / 2.0) + 2000.0;  // + fill/epilogue
+    double eff = (c.cg == 2) ? 1.0 : 0.65;
+    if (c.bn_cta == 32) eff *= 0.8;
+    // Wasted MMA work on zero-filled tile padding is already in `waves`.
+    const double t = static_cast<double>(waves) * per_tile / eff;
+    if (t < best_t * 0.999) {
+      best_t = t;
+      best = c;
+    }
+  }
+  return best;
+}
+
+}  // namespace tmk

@@ -1,0 +1,37 @@
+// tm_internal.h -- internal interfaces between the C-ABI layer and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/tm.h"
+
+namespace tmk {
+
+struct GemmArgs {
+  int64_t m, n, k;
+  float alpha, beta;
+  const float* A;
+  int64_t lda;
+  const float* B;
+  int64_t ldb;
+  float* C;
+  int64_t ldc;
+};
+
+// Tensor-core configuration: CTA group (1 or 2), B columns per CTA (32/64/128),
+// 3xTF32 (true) or single-pass TF32 (false, bring-up only).
+struct TcChoice {
+  int cg;
+  int bn_cta;
+  bool split3;
+};
+
+tm_status launch_tc(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream);
+tm_status launch_simt(const GemmArgs& a, cudaStream_t stream);
+tm_status launch_scale(int64_t m, int64_t n, float beta, float* C, int64_t ldc, cudaStream_t stream);
+
+// Picks the tensor-core configuration for a shape (planner, plan.cpp).
+TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms);
+
+}  // namespace tmk

@@ -1,0 +1,123 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/tm.h declares, validates arguments on the host before any CUDA
+call, dispatches paths by alignment, and has no CPU fallback."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1804_10694_b200 as tm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    with open(os.path.join(ROOT, "include", "tm.h")) as f:
+        src = f.read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tm_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported():
+    declared = _declared_symbols()
+    assert len(declared) >= 15
+    assert sorted(tm.EXPORTED_SYMBOLS) == declared
+    L = ctypes.CDLL(tm.lib_path)
+    for name in declared:
+        assert getattr(L, name) is not None, name
+
+
+def test_library_is_sm100a_only():
+    """The .so carries only sm_100a SASS (no PTX for JIT, no other arch)."""
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", tm.lib_path], capture_output=True,
+                         text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_status_strings_and_version():
+    assert tm.status_string(0) == "TM_OK"
+    assert tm.status_string(1) == "TM_ERR_INVALID_VALUE"
+    assert tm.status_string(2) == "TM_ERR_UNSUPPORTED_DEVICE"
+    assert tm.lib.tm_get_version() >= 100
+
+
+def _ex(m, n, k, alpha=1.0, A=16, lda=None, B=16, ldb=None, beta=0.0, C=1 << 20, ldc=None, algo=0):
+    lda = max(k, 1) if lda is None else lda
+    ldb = max(n, 1) if ldb is None else ldb
+    ldc = max(n, 1) if ldc is None else ldc
+    return tm.lib.tm_sgemm_ex(m, n, k, alpha, ctypes.c_void_p(A), lda, ctypes.c_void_p(B), ldb, beta,
+                              ctypes.c_void_p(C), ldc, None, algo)
+
+
+@pytest.mark.parametrize("args", [
+    dict(m=-1, n=4, k=4),
+    dict(m=4, n=-1, k=4),
+    dict(m=4, n=4, k=-1),
+    dict(m=4, n=4, k=8, lda=7),          # lda < k
+    dict(m=4, n=8, k=4, ldb=7),          # ldb < n
+    dict(m=4, n=8, k=4, ldc=7),          # ldc < n
+    dict(m=4, n=4, k=4, A=0),            # NULL A while alpha != 0
+    dict(m=4, n=4, k=4, B=0),            # NULL B
+    dict(m=4, n=4, k=4, C=0),            # NULL C
+    dict(m=4, n=4, k=4, A=1 << 20),      # C overlaps A
+    dict(m=4, n=4, k=4, algo=9),         # unknown algo
+    dict(m=4, n=4, k=4, C=(1 << 20) + 4, algo=1),  # TF32X3 forced on misaligned C
+])
+def test_invalid_arguments_rejected_on_host(args):
+    assert _ex(**args) == 1  # TM_ERR_INVALID_VALUE, before any CUDA call
+
+
+def test_noop_needs_no_device():
+    assert _ex(0, 5, 5) == 0
+    assert _ex(5, 0, 5) == 0
+
+
+def test_no_cpu_fallback():
+    """Valid arguments on a machine without a usable sm_100 device must fail,
+    never silently compute on the host."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    assert _ex(8, 8, 8) in (2, 3)  # UNSUPPORTED_DEVICE or CUDA error
+
+
+def test_plan_dispatch_by_alignment():
+    # aligned pointers + ld % 4 == 0 -> tensor cores; otherwise SIMT (never an error under AUTO)
+    assert tm.plan_name(64, 64, 64, 1.0, 0.0, 1 << 12, 64, 1 << 16, 64, 1 << 24, 64) == "tf32x3"
+    assert tm.plan_name(64, 64, 64, 1.0, 0.0, (1 << 12) + 4, 64, 1 << 16, 64, 1 << 24, 64) == "simt"
+    assert tm.plan_name(64, 63, 64, 1.0, 0.0, 1 << 12, 64, 1 << 16, 63, 1 << 24, 63) == "simt"
+    assert tm.plan_name(64, 64, 64, 1.0, 0.0, 1 << 12, 64, 1 << 16, 64, 1 << 24, 64, algo=2) == "simt"
+    assert tm.plan_name(64, 64, 64, 1.0, 0.0, 1 << 12, 64, 1 << 16, 64, 1 << 24, 64, algo=3) == "tf32x1"
+    # special cases
+    assert tm.plan_name(64, 64, 64, 0.0, 0.5, 0, 64, 0, 64, 1 << 24, 64) == "scale"
+    assert tm.plan_name(64, 64, 0, 1.0, 0.5, 0, 1, 0, 64, 1 << 24, 64) == "scale"
+    assert tm.plan_name(0, 64, 64, 1.0, 0.5, 0, 64, 0, 64, 0, 64) == "noop"
+    assert tm.plan_name(-1, 64, 64) == "invalid"
+
+
+def test_dist_rows_partition():
+    for m in [0, 1, 5, 1060, 16384, 16387]:
+        for P in [1, 2, 3, 4, 8]:
+            seen = []
+            for r in range(P):
+                r0, nr = tm.dist_rows(m, P, r)
+                seen.extend(range(r0, r0 + nr))
+            assert seen == list(range(m))
+    with pytest.raises(tm.TmError):
+        tm.dist_rows(10, 0, 0)
+    with pytest.raises(tm.TmError):
+        tm.dist_rows(10, 2, 2)
+
+
+def test_product_package_never_imports_oracle():
+    """The product path shares no code with the oracle."""
+    pkg = os.path.join(ROOT, "paper_1804_10694_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
+                with open(os.path.join(dirpath, f)) as fh:
+                    src = fh.read()
+                assert "oracle" not in src.replace("# no oracle", ""), f
