@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""bench.py -- sgemm throughput on B200 (driver contract: one JSON line on rank 0).
+
+Default workload (BASELINE.json configs[4], the config the metric is quoted on
+"at 1/2/4/8 B200"): C = alpha*A*B + beta*C, M = N = K = 16384, fp32, alpha=1.5,
+beta=0.5, row-block sharded over the N GPUs with B broadcast from rank 0 via
+NCCL (strong scaling: total work fixed).  At N = 1 it is one tm_sgemm call.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C1|C2|C3|C3b|C4|C5] [--algo auto|tf32x3|simt]
+
+A "step" is one pass of the whole hot path (one sgemm over the workload) with
+inputs resident in HBM; `e2e` repeats the metric through tm_sgemm_host (host
+buffers, copies inside the timed region).  `--impl reference` times the CPU
+oracle (the tier's reference arm) on a bounded row sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sgemm GFLOP/s and % of TF32/FP32 roofline at 1/2/4/8 B200 vs CPU oracle"
+ALGOS = {"auto": 0, "tf32x3": 1, "simt": 2}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def roofline_peak(path, peaks):
+    """(bound, peak, unit, note).  3xTF32: measured bf16 dense peak x nominal
+    tf32/bf16 ratio (1.1/2.25) / 3 MMAs per fp32 product.  SIMT: FFMA peak from
+    unit counts (148 SMs x 128 FP32 lanes x 2 flop x max SM clock)."""
+    if path == "simt":
+        return "alu", 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12, "TFLOP/s", "148 SM x 128 FFMA/clk x 2 x sm_max_mhz"
+    tf32 = peaks["bf16_tflops"] * (1.1 / 2.25)
+    return "tensor", tf32 / 3.0, "TFLOP/s", f"{peaks['source']} bf16 {peaks['bf16_tflops']} x 1.1/2.25 (tf32) / 3 (3xTF32)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload(name):
+    import seeded_inputs as si
+    m, n, k = si.CONFIGS[name]
+    desc = {
+        "C1": "sgemm 64^3 alpha=1.5 beta=0.5",
+        "C2": "sgemm 1060^3 (partial tiles)",
+        "C3": "sgemm 4096^3",
+        "C3b": "sgemm 8192^3 (north_star target size)",
+        "C4": "conv-shaped im2col sgemm 50176x64x576",
+        "C5": "sgemm 16384^3 row-block sharded, B broadcast via NCCL",
+    }[name]
+    return m, n, k, desc
+
+
+def make_inputs(name, m, n, k, rank_rows=None, device="cuda"):
+    """Seeded synthetic inputs generated on the device (torch Philox, U[-1,1))
+    for the big configs -- the parity tests use the numpy generator at the
+    same shapes; throughput does not depend on the values."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(1804)
+    r0, rows = rank_rows if rank_rows else (0, m)
+    A = torch.rand((rows, k), generator=g, device=device, dtype=torch.float32) * 2 - 1
+    B = torch.rand((k, n), generator=g, device=device, dtype=torch.float32) * 2 - 1
+    C = torch.rand((rows, n), generator=g, device=device, dtype=torch.float32) * 2 - 1
+    return A, B, C
+
+
+def cpu_oracle_sample(m, n, k, alpha, beta, budget_s=15.0, extra_rows=()):
+    """Times the CPU oracle (as it stands) on a row sample of the workload;
+    returns (GFLOP/s extrapolated, cores, sample description)."""
+    import numpy as np
+    import oracle
+    import seeded_inputs as si
+    g = si.rng(99)
+    B = si.uniform(g, (k, n))
+    cores = oracle.get_threads()
+    # calibrate on `cores` rows, then size the sample to ~budget_s
+    rows = np.arange(min(m, cores), dtype=np.int64)
+    A = si.uniform(g, (m if m <= 4 * cores else len(rows), k))
+    C0 = si.uniform(g, (A.shape[0], n))
+    t0 = time.perf_counter()
+    oracle.sgemm(alpha, A, B, beta, C0, rows=rows, m=A.shape[0])
+    t1 = time.perf_counter() - t0
+    target = int(max(len(rows), min(m, len(rows) * budget_s / max(t1, 1e-3))))
+    target = max(cores, target - target % cores) if target > cores else target
+    A = si.uniform(g, (target, k))
+    C0 = si.uniform(g, (target, n))
+    t0 = time.perf_counter()
+    oracle.sgemm(alpha, A, B, beta, C0)
+    dt = time.perf_counter() - t0
+    gflops = 2.0 * target * n * k / dt / 1e9
+    return gflops, cores, f"{target} rows x {n} cols x K={k} of the {m}x{n}x{k} workload ({dt:.1f} s)"
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the host cores, bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import seeded_inputs as si
+    m, n, k, desc = workload(args.config)
+    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    vals = []
+    sample = cores = None
+    for i in range(args.warmup + args.steps):
+        v, cores, sample = cpu_oracle_sample(m, n, k, si.ALPHA, si.BETA, budget_s=budget)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    flops = 2.0 * m * n * k
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(flops / (value * 1e9) * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded U[-1,1) fp32 inputs)",
+        "config": {"workload": desc, "m": m, "n": n, "k": k, "alpha": si.ALPHA, "beta": si.BETA},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": sample + "; ms_per_step extrapolated to the full workload"},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C3b", "C4", "C5"])
+    ap.add_argument("--algo", default="auto", choices=list(ALGOS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1804_10694_b200 as tm
+    import seeded_inputs as si
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = load_peaks()
+    m, n, k, desc = workload(args.config)
+    alpha, beta = si.ALPHA, si.BETA
+    algo = ALGOS[args.algo]
+    stream = torch.cuda.current_stream()
+
+    if args.config == "C4":
+        A_np, B_np, C_np = si.im2col_conv()
+        A, B, C = (torch.from_numpy(x).cuda() for x in (A_np, B_np, C_np))
+        r0, rows = 0, m
+    else:
+        r0, rows = tm.dist_rows(m, world, rank)
+        A, B, C = make_inputs(args.config, m, n, k, (r0, rows))
+    comm = tm.Comm(rank, world) if world > 1 else None
+    in_bytes = 4 * (m * k + k * n + m * n)
+    small = in_bytes < 2 * 126 * 2 ** 20  # inputs fit in L2: flush between iterations
+    flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda") if small else None
+
+    def step():
+        if comm is None:
+            tm.sgemm_ex(A, B, C, alpha, beta, algo)
+        else:
+            comm.sgemm(m, n, k, A, B, C, alpha, beta, root=0)
+
+    path = tm.plan_name(rows, n, k, alpha, beta, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+                        C.data_ptr(), C.stride(0), algo)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    per_step = [a.elapsed_time(b) for a, b in ev]  # ms, device time of each step's hot path
+    total_ms = sum(per_step)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    flops = 2.0 * m * n * k
+    value = flops * args.steps / (total_ms * 1e-3) / 1e9  # GFLOP/s, whole job
+
+    # roofline of the dominant kernel (the GEMM), from this rank's live event times
+    kernel = "simt" if path == "simt" else "tf32x3"
+    bound, peak, unit, peak_note = roofline_peak(kernel, peaks)
+    my_flops = 2.0 * rows * n * k
+    my_ms = statistics.mean(per_step)
+    if args.config == "C4":
+        bound, unit = "hbm", "GB/s"
+        peak = peaks["hbm_gbs"]
+        algo_bytes = 4 * (m * k + k * n + (2 if beta != 0 else 1) * m * n)
+        achieved = algo_bytes / (my_ms * 1e-3) / 1e9
+        peak_note = peaks["source"] + " hbm_gbs"
+    else:
+        achieved = my_flops / (my_ms * 1e-3) / 1e12
+    roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": None, "kernel": f"k_sgemm_tc ({path})" if kernel != "simt"
+            else "k_sgemm_simt", "peak_source": peak_note}
+    if bound == "tensor":
+        sus = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / 3.0
+        roof["frac_of_sustained_peak"] = round(achieved / sus, 4)
+    launches = args.steps * (1 if comm is None else max(1, min(8, k // 512)))
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core, fp32 accumulate)"
+        if kernel != "simt" else "f32", "data": "synthetic (seeded U[-1,1) fp32, device-generated)",
+        "config": {"workload": desc, "m": m, "n": n, "k": k, "alpha": alpha, "beta": beta, "path": path,
+                   "rows_per_rank": rows, "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2, no flush" if not small else "L2 flushed (512 MiB write) between steps"},
+        "roofline": roof, "gpu_launches": launches, "clocks": clocks.summary(),
+    }
+
+    # e2e through the public API with host buffers (copies inside the timed region)
+    if not args.no_e2e:
+        line["e2e"] = measure_e2e(tm, torch, dist, world, rank, m, n, k, rows, alpha, beta, algo, comm, args)
+
+    if rank == 0 and not args.no_cpu and world == 1:
+        v, cores, sample = cpu_oracle_sample(m, n, k, alpha, beta, budget_s=15.0)
+        line["cpu_baseline"] = {"value": round(v, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                                "sample": sample}
+    if comm is not None:
+        comm.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_e2e(tm, torch, dist, world, rank, m, n, k, rows, alpha, beta, algo, comm, args):
+    steps = max(1, min(args.steps, 3))
+    hA = torch.empty((rows, k), dtype=torch.float32, pin_memory=True).uniform_(-1, 1)
+    hB = torch.empty((k, n), dtype=torch.float32, pin_memory=True).uniform_(-1, 1)
+    hC = torch.empty((rows, n), dtype=torch.float32, pin_memory=True).uniform_(-1, 1)
+    if comm is None:
+        def step():
+            tm.sgemm_host(hA, hB, hC, alpha, beta, algo)
+        h2d = 4 * (rows * k + k * n + rows * n)
+    else:
+        dA = torch.empty((rows, k), dtype=torch.float32, device="cuda")
+        dB = torch.empty((k, n), dtype=torch.float32, device="cuda")
+        dC = torch.empty((rows, n), dtype=torch.float32, device="cuda")
+
+        def step():
+            dA.copy_(hA, non_blocking=True)
+            if rank == 0:
+                dB.copy_(hB, non_blocking=True)
+            dC.copy_(hC, non_blocking=True)
+            comm.sgemm(m, n, k, dA, dB, dC, alpha, beta, root=0)
+            hC.copy_(dC, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        h2d = 4 * (rows * k + (k * n if rank == 0 else 0) + rows * n)
+    step()  # warm-up (workspace allocation)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    return {"value": round(2.0 * m * n * k * steps / dt / 1e9, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": 4 * rows * n, "steps": steps,
+            "note": "tm_sgemm_host: pinned host A,B,C -> device, GEMM, C -> host, per step (host wall clock, synchronised)"
+            if comm is None else "pinned H2D of shards + tm_sgemm_dist + D2H of C shard (host wall clock, max over ranks)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -142,6 +142,13 @@ tm_status tm_comm_rank(tm_comm_t comm, int* rank, int* nranks);
  *   rows = m/P + (rank < m%P),  row0 = rank*(m/P) + min(rank, m%P). */
 tm_status tm_dist_rows(int64_t m, int nranks, int rank, int64_t* row0, int64_t* rows);
 
+/* K-chunk schedule of tm_sgemm_dist (host-only, no device): number of chunks
+ * B is broadcast in for this (k, nranks), and chunk `idx`'s K range
+ * [*k0, *k0 + *kr).  Chunks tile [0, k) exactly once, in order; every chunk
+ * but the last starts at a multiple of 32.  idx < 0 only returns the count
+ * in *k0. */
+tm_status tm_dist_chunk(int64_t k, int nranks, int idx, int64_t* k0, int64_t* kr);
+
 /* Collective: all ranks call with identical m, n, k, alpha, beta, root.
  *   A_local: rows x k (lda), C_local: rows x n (ldc), rows from tm_dist_rows.
  *   B: k x n (ldb); valid on `root`; on other ranks a caller-owned k*ldb

@@ -27,7 +27,7 @@ lib_path = os.path.join(_PKG, "_lib", "libtm.so")
 EXPORTED_SYMBOLS = [
     "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
     "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
-    "tm_dist_rows", "tm_sgemm_dist", "tm_sgemm_dist_allgather", "tm_comm_bytes_received",
+    "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_allgather", "tm_comm_bytes_received",
 ]
 
 
@@ -53,6 +53,7 @@ def _load():
     L.tm_status_string.argtypes = [ci]
     L.tm_status_string.restype = ctypes.c_char_p
     L.tm_dist_rows.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.tm_dist_chunk.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.tm_comm_get_unique_id.argtypes = [vp]
     L.tm_comm_init.argtypes = [ctypes.POINTER(vp), ci, ci, vp]
     L.tm_comm_destroy.argtypes = [vp]
@@ -176,6 +177,24 @@ def dist_rows(m: int, nranks: int, rank: int):
     r0, nr = ctypes.c_int64(), ctypes.c_int64()
     _check(lib.tm_dist_rows(m, nranks, rank, ctypes.byref(r0), ctypes.byref(nr)), "tm_dist_rows")
     return r0.value, nr.value
+
+
+def dist_chunks(k: int, nranks: int):
+    """K-chunk schedule of the distributed broadcast: list of (k0, kr)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.tm_dist_chunk(k, nranks, -1, ctypes.byref(a), ctypes.byref(b)), "tm_dist_chunk")
+    out = []
+    for i in range(a.value):
+        _check(lib.tm_dist_chunk(k, nranks, i, ctypes.byref(a), ctypes.byref(b)), "tm_dist_chunk")
+        out.append((a.value, b.value))
+    return out
+
+
+def unique_id() -> bytes:
+    """A fresh NCCL unique id (host-only)."""
+    uid = (ctypes.c_ubyte * 128)()
+    _check(lib.tm_comm_get_unique_id(ctypes.byref(uid)), "tm_comm_get_unique_id")
+    return bytes(uid)
 
 
 class Comm:

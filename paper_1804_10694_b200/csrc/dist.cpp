@@ -155,6 +155,22 @@ static int choose_chunks(int64_t k, int nranks) {
   return static_cast<int>(c);
 }
 
+tm_status tm_dist_chunk(int64_t k, int nranks, int idx, int64_t* k0, int64_t* kr) {
+  if (k < 0 || nranks < 1 || !k0 || !kr) return TM_ERR_INVALID_VALUE;
+  const int nch = choose_chunks(k, nranks);
+  const int64_t kc = ((k + nch - 1) / nch + 31) / 32 * 32;
+  const int64_t count = k == 0 ? 0 : (k + kc - 1) / kc;
+  if (idx < 0) {
+    *k0 = count;
+    *kr = kc;
+    return TM_OK;
+  }
+  if (idx >= count) return TM_ERR_INVALID_VALUE;
+  *k0 = idx * kc;
+  *kr = (*k0 + kc <= k) ? kc : k - *k0;
+  return TM_OK;
+}
+
 tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha, const float* A_local,
                         int64_t lda, float* B, int64_t ldb, int root, float beta, float* C_local, int64_t ldc,
                         void* stream_) {
@@ -169,8 +185,9 @@ tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float a
     return tm_sgemm(rows, n, k, alpha, A_local, lda, B, ldb, beta, C_local, ldc, stream);
   }
   if (!B || ldb < (n > 1 ? n : 1)) return TM_ERR_INVALID_VALUE;
-  const int nch = choose_chunks(k, comm->nranks);
-  const int64_t kc = ((k + nch - 1) / nch + 31) / 32 * 32;
+  int64_t nchunks = 0, kc = 0;
+  tm_dist_chunk(k, comm->nranks, -1, &nchunks, &kc);
+  if (nchunks > kMaxChunks) return TM_ERR_INTERNAL;
   if (cudaEventRecord(comm->ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
   if (cudaStreamWaitEvent(comm->stream, comm->ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
   int used = 0;

@@ -203,18 +203,27 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------- descriptors
-// Shared-memory matrix descriptor (tcgen05), SWIZZLE_128B:
+// Shared-memory matrix descriptor (tcgen05):
 //   [0,14)  start address >> 4      [16,30) leading byte offset >> 4
 //   [32,46) stride byte offset >> 4 [46,48) version = 1 (sm_100)
 //   [49,52) base offset = 0         [52]    LBO mode = 0
-//   [61,64) layout: 2 = SWIZZLE_128B
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+//   [61,64) layout type: 2 = SWIZZLE_128B (16-B chunks XOR row%8 within 128 B),
+//           1 = SWIZZLE_128B_BASE32B (32-B chunks XOR row%4 within 128 B).
+// Layouts used here (probed on B200, scripts/tc_probe.py):
+//   A, K-major, SWIZZLE_128B: rows of 128 B (32 tf32 of K), SBO = 1024 (8 rows), LBO unused.
+//   B, MN-major, SWIZZLE_128B_BASE32B: K-rows of 128 B (32 tf32 of N), SBO = 512
+//      (next 4 K-rows), LBO = stride between 32-column atoms.  kind::tf32 accepts
+//      MN-major operands only in this layout; plain SWIZZLE_128B / no-swizzle
+//      MN-major tf32 descriptors silently produce zeros.
+constexpr uint32_t kLayoutSW128 = 2;
+constexpr uint32_t kLayoutSW128Base32B = 1;
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
   d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
   d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
   d |= static_cast<uint64_t>(1) << 46;
-  d |= static_cast<uint64_t>(2) << 61;
+  d |= static_cast<uint64_t>(layout & 7u) << 61;
   return d;
 }
 

@@ -20,7 +20,7 @@
 //
 // Warp roles (384 threads, 1 CTA per SM, persistent over tiles):
 //   warp 0      TMA producer (one lane): A box 128x32 (K-major, SW128),
-//               B boxes 32x32 (MN-major, SW128) into the raw ring.
+//               B boxes 32x32 (MN-major, SW128 with 32-B atoms) into the raw ring.
 //   warp 1      MMA issuer (one lane, leader CTA only): 3 tcgen05.mma per
 //               K=8 step into a double-buffered TMEM accumulator.
 //   warp 2      TMEM allocator.
@@ -237,14 +237,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int ks = 0; ks < kBK / 8; ++ks) {
             // A: K-major SW128, K step of 8 tf32 = 32 B inside the swizzle row.
-            // B: MN-major SW128, K step of 8 rows = one 1024-B swizzle atom;
-            //    32-column atoms are 4096 B apart (LBO).
-            const uint64_t aH = ptx::sdesc_sw128(rawA_s + s * Cfg::kABytes + ks * 32, 16, 1024);
-            const uint64_t bH = ptx::sdesc_sw128(rawB_s + s * Cfg::kBBytes + ks * 1024, 4096, 1024);
+            // B: MN-major SW128_BASE32B, K step of 8 rows = 1024 B (two 512-B
+            //    atoms, SBO); 32-column atoms are 4096 B apart (LBO).
+            const uint64_t aH = ptx::sdesc(rawA_s + s * Cfg::kABytes + ks * 32, 16, 1024, ptx::kLayoutSW128);
+            const uint64_t bH = ptx::sdesc(rawB_s + s * Cfg::kBBytes + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
             const uint32_t first = (kb | ks) != 0;
             if constexpr (SPLIT3) {
-              const uint64_t aL = ptx::sdesc_sw128(loA_s + sl * Cfg::kABytes + ks * 32, 16, 1024);
-              const uint64_t bL = ptx::sdesc_sw128(loB_s + sl * Cfg::kBBytes + ks * 1024, 4096, 1024);
+              const uint64_t aL = ptx::sdesc(loA_s + sl * Cfg::kABytes + ks * 32, 16, 1024, ptx::kLayoutSW128);
+              const uint64_t bL = ptx::sdesc(loB_s + sl * Cfg::kBBytes + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
               ptx::mma_tf32<CG>(d, aL, bH, idesc, first);
               ptx::mma_tf32<CG>(d, aH, bL, idesc, 1u);
               ptx::mma_tf32<CG>(d, aH, bH, idesc, 1u);
@@ -366,9 +366,9 @@ EncodeTiledFn get_encode() {
 }
 
 // 2-D fp32 row-major tensor (rows x cols, leading dimension ld elements),
-// box = box_cols x box_rows, 128-byte swizzle, OOB elements read as zero.
+// box = box_cols x box_rows, 128-byte swizzle span, OOB elements read as zero.
 bool encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_cols,
-               uint32_t box_rows) {
+               uint32_t box_rows, CUtensorMapSwizzle swizzle) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -376,7 +376,7 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, 
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -393,8 +393,8 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t stream) {
   }
   CUtensorMap tmA, tmB;
   // A: m x k, box 32 (k) x 128 (rows).  B: k x n, box 32 (n) x 32 (k rows).
-  if (!encode_2d(&tmA, a.A, a.m, a.k, a.lda, kBK, kBMCta)) return TM_ERR_INTERNAL;
-  if (!encode_2d(&tmB, a.B, a.k, a.n, a.ldb, 32, kBK)) return TM_ERR_INTERNAL;
+  if (!encode_2d(&tmA, a.A, a.m, a.k, a.lda, kBK, kBMCta, CU_TENSOR_MAP_SWIZZLE_128B)) return TM_ERR_INTERNAL;
+  if (!encode_2d(&tmB, a.B, a.k, a.n, a.ldb, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return TM_ERR_INTERNAL;
   TcParams p;
   p.m = static_cast<int>(a.m);
   p.n = static_cast<int>(a.n);
