@@ -28,8 +28,12 @@ TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms) {
     const int64_t units = num_sms / c.cg;
     const int64_t waves = (tiles + units - 1) / units;
     double per_tile = static_cast<double>(kb) * 4.0 * 3.0 * (c.cg * c.bn_cta / 2.0) + 2000.0;  // + fill/epilogue
-    double eff = (c.cg == 2) ? 1.0 : 0.65;
-    if (c.bn_cta == 32) eff *= 0.8;
+    // Sustained MMA efficiency per configuration, measured on B200 at 8192^3
+    // (DESIGN.md "Planner"): narrower tiles re-read A from shared memory more
+    // often per MMA and a 1-CTA tile reads all of B from one SM.
+    double eff = 1.0;
+    if (c.cg == 2) eff = (c.bn_cta == 128) ? 1.0 : (c.bn_cta == 64) ? 0.6 : 0.35;
+    else eff = (c.bn_cta == 128) ? 0.75 : (c.bn_cta == 64) ? 0.45 : 0.25;
     // Wasted MMA work on zero-filled tile padding is already in `waves`.
     const double t = static_cast<double>(waves) * per_tile / eff;
     if (t < best_t * 0.999) {

@@ -3,37 +3,43 @@
 // Computes C = alpha*A*B + beta*C in fp32-faithful accuracy:
 // every fp32 operand x is split as x = hi + lo with hi = x truncated to TF32
 // (the tensor core itself ignores the low 13 mantissa bits of a raw fp32
-// operand in kind::tf32, so the raw TMA tile serves as hi) and
+// operand in kind::tf32 -- probed -- so the raw TMA tile serves as hi) and
 // lo = rna_tf32(x - hi) (exact subtraction, one rounding), and
 //     A*B ~= A_lo*B_hi + A_hi*B_lo + A_hi*B_hi        (lo*lo dropped)
-// accumulated in fp32 in TMEM.  See DESIGN.md "3xTF32" for the error bound.
+// accumulated in fp32.  The tensor core accumulates with round-toward-zero
+// (probed), so partial sums over K_c = 128 live in TMEM and are promoted into
+// round-to-nearest fp32 register accumulators ("K_c promotion", K_c = 128); see
+// DESIGN.md "3xTF32 accuracy".
 //
 // Structure (the paper's GPU gemm optimisations, PAPER.md:69-71, 780, 830-831,
 // mapped to Blackwell): two-level tiling = persistent cluster tiles (tiling map
 // i0 = floor(i/BM), i1 = i % BM) x K-blocks of 32;
 // "data movement between global, shared and register memory" = TMA into a
-// multi-stage shared-memory ring + TMEM accumulators; "array packing" = the
-// in-smem lo split; "synchronization primitives" = mbarrier full/empty rings;
-// "separation of full and partial tiles" = TMA zero-fill for loads plus an
-// explicit full-tile (unpredicated vector) / partial-tile (predicated)
-// epilogue that fuses alpha/beta.
+// multi-stage shared-memory ring + TMEM partials + register accumulators;
+// "array packing" = the in-smem lo split; "synchronization primitives" =
+// mbarrier full/empty rings; "separation of full and partial tiles" = TMA
+// zero-fill for loads plus an explicit full-tile (unpredicated vector) /
+// partial-tile (predicated) epilogue that fuses alpha/beta.
 //
-// Warp roles (384 threads, 1 CTA per SM, persistent over tiles):
-//   warp 0      TMA producer (one lane): A box 128x32 (K-major, SW128),
-//               B boxes 32x32 (MN-major, SW128 with 32-B atoms) into the raw ring.
-//   warp 1      MMA issuer (one lane, leader CTA only): 3 tcgen05.mma per
-//               K=8 step into a double-buffered TMEM accumulator.
-//   warp 2      TMEM allocator.
-//   warps 4-7   epilogue: tcgen05.ld -> alpha/beta -> global (warp w%4 owns
-//               TMEM lanes 32*(w%4)..+31).
-//   warps 8-11  split: raw tile -> lo tile (same swizzled layout, so the MMA
+// Warp roles (512 threads = 4 warpgroups, 1 CTA per SM, persistent):
+//   WG0 warp 0  TMA producer (one lane): A box 128x32 (K-major, SW128),
+//               B boxes 32x32 (MN-major, SW128 with 32-B atoms) -> raw ring.
+//       warp 1  MMA issuer (one lane, leader CTA only): 3 tcgen05.mma per K=8
+//               step into one of two TMEM partial buffers (ping-pong per K_c).
+//       warp 2  TMEM allocator.
+//   WG1         split: raw tile -> lo tile (same swizzled layout, so the MMA
 //               descriptors for lo differ from hi only in the start address).
+//   WG2, WG3    promotion + epilogue: drain each finished TMEM partial into
+//               fp32 registers (RN adds), then alpha/beta and store C.  Warp w
+//               owns TMEM lanes 32*(w%4).. (rows) and column half (w-8)/4.
 // CG == 2 runs a CTA pair (cta_group::2): tile 256 x (2*BN_CTA), A split along
 // M and B along N between the two CTAs' shared memories; CTA 0 issues MMAs.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ptx.cuh"
 #include "tm_internal.h"
@@ -42,9 +48,11 @@ namespace tmk {
 
 constexpr int kBK = 32;            // K elements per stage (= one 128-byte swizzle row)
 constexpr int kBMCta = 128;        // A rows per CTA
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kSplitThreads = 128;
-constexpr int kGroupM = 8;         // raster: tile-rows per group (L2 reuse)
+constexpr int kEpiWarps = 8;
+constexpr int kKcBlocksDefault = 4;   // K_c = 4 * 32 = 128: RZ partial length before RN promotion
+constexpr int kGroupMDefault = 8;     // raster: tile-rows per group (L2 reuse)
 
 template <int BN_CTA>
 struct StageCfg;
@@ -58,15 +66,15 @@ struct StageCfg<32> { static constexpr int kRaw = 6, kLo = 3; };
 template <int CG, int BN_CTA, bool SPLIT3>
 struct TcCfg {
   static constexpr int kRaw = StageCfg<BN_CTA>::kRaw;
-  static constexpr int kLo = SPLIT3 ? StageCfg<BN_CTA>::kLo : 1;
+  static constexpr int kLo = StageCfg<BN_CTA>::kLo;  // ready/empty_lo ring depth (no lo smem if !SPLIT3)
   static constexpr int kABytes = kBMCta * kBK * 4;   // 16 KiB
   static constexpr int kBBytes = kBK * BN_CTA * 4;   // BN_CTA/32 boxes of 4 KiB
   static constexpr int kMmaM = kBMCta * CG;
   static constexpr int kMmaN = BN_CTA * CG;
   static constexpr int kTileM = kMmaM;
   static constexpr int kTileN = kMmaN;
-  static constexpr int kAccCols = kMmaN;
-  static constexpr int kTmemCols = (2 * kAccCols <= 32) ? 32 : (2 * kAccCols <= 64) ? 64 : (2 * kAccCols <= 128) ? 128 : (2 * kAccCols <= 256) ? 256 : 512;
+  static constexpr int kCols = kMmaN / 2;            // columns per promotion warp
+  static constexpr int kTmemCols = (2 * kMmaN <= 32) ? 32 : (2 * kMmaN <= 64) ? 64 : (2 * kMmaN <= 128) ? 128 : (2 * kMmaN <= 256) ? 256 : 512;
   static constexpr int kRawBytes = kRaw * (kABytes + kBBytes);
   static constexpr int kLoBytes = SPLIT3 ? kLo * (kABytes + kBBytes) : 0;
   static constexpr int kNumBars = 2 * kRaw + 2 * kLo + 4;
@@ -76,71 +84,87 @@ struct TcCfg {
 struct TcParams {
   int m, n, k;
   int tiles_m, tiles_n, num_tiles, kblocks;
+  int kc_blocks;  // K-blocks per TMEM partial (K_c / 32)
+  int group_m;    // raster group height in tiles
   float alpha, beta;
   float* C;
   long long ldc;
 };
 
+// lo part of the 3xTF32 split of one fp32 value x (bit pattern):
+//   hi = x with the low 13 mantissa bits cleared (what kind::tf32 reads from a
+//        raw fp32 operand, probed: tests/test_probes.py),
+//   d  = x - hi, exact in fp32,
+//   lo = d rounded to TF32, round-to-nearest ties-away on the magnitude:
+//        (bits(d) + 0x1000) & ~0x1FFF  (integer form of cvt.rna.tf32.f32 for
+//        finite d; the carry into the exponent is the correct rounding).
 __device__ __forceinline__ uint32_t tf32_lo_bits(uint32_t x) {
-  const float xf = __uint_as_float(x);
   const float hi = __uint_as_float(x & 0xFFFFE000u);
-  const float d = __fsub_rn(xf, hi);  // exact: hi holds the leading bits of x
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(d));
-  return r;
+  const float d = __fsub_rn(__uint_as_float(x), hi);
+  return (__float_as_uint(d) + 0x1000u) & 0xFFFFE000u;
+}
+__device__ __forceinline__ uint4 tf32_lo4(uint4 v) {
+  return make_uint4(tf32_lo_bits(v.x), tf32_lo_bits(v.y), tf32_lo_bits(v.z), tf32_lo_bits(v.w));
 }
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm_, int& tn_) {
-  const int per_group = kGroupM * tiles_n;
+// Split one smem tile of BYTES (raw -> lo, same offsets, so the same swizzled
+// layout) with 128 threads, 8 loads in flight per thread.
+template <int BYTES>
+__device__ __forceinline__ void split_tile(uint32_t src, uint32_t dst, int st) {
+  constexpr int kIters = BYTES / 16 / kSplitThreads;
+  constexpr int kBatch = kIters < 8 ? kIters : 8;
+#pragma unroll
+  for (int b = 0; b < kIters; b += kBatch) {
+    uint4 v[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) v[i] = ptx::lds128(src + ((b + i) * kSplitThreads + st) * 16);
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) ptx::sts128(dst + ((b + i) * kSplitThreads + st) * 16, tf32_lo4(v[i]));
+  }
+}
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group_m, int& tm_, int& tn_) {
+  const int per_group = group_m * tiles_n;
   const int g = t / per_group;
-  const int first_m = g * kGroupM;
-  const int gsize = min(tiles_m - first_m, kGroupM);
+  const int first_m = g * group_m;
+  const int gsize = min(tiles_m - first_m, group_m);
   const int r = t - g * per_group;
   tm_ = first_m + r % gsize;
   tn_ = r / gsize;
 }
 
 // ------------------------------------------------------------------ epilogue
-// Full tile: every row/column of this thread's 16-column chunk is inside C;
+// Full tile: all KCOLS columns of this thread's row are inside C:
 // unpredicated 16-byte vector accesses (ldc % 4 == 0 and C 16-B aligned are
-// preconditions of this path).
-__device__ __forceinline__ void epi_full16(float* __restrict__ crow, const uint32_t (&r)[16], float alpha,
-                                           float beta) {
-  float4* c4 = reinterpret_cast<float4*>(crow);
-  if (beta == 0.0f) {
+// preconditions of this path).  Partial tile: row/column predicates, nothing
+// outside m x n is touched.
+template <int KCOLS>
+__device__ __forceinline__ void epi_store(float* __restrict__ crow, const float (&acc)[KCOLS], bool full_row,
+                                          int ncols, float alpha, float beta) {
+  if (full_row) {
+    float4* c4 = reinterpret_cast<float4*>(crow);
+    if (beta == 0.0f) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float4 o;
-      o.x = alpha * __uint_as_float(r[4 * q + 0]);
-      o.y = alpha * __uint_as_float(r[4 * q + 1]);
-      o.z = alpha * __uint_as_float(r[4 * q + 2]);
-      o.w = alpha * __uint_as_float(r[4 * q + 3]);
-      c4[q] = o;
+      for (int q = 0; q < KCOLS / 4; ++q)
+        c4[q] = make_float4(alpha * acc[4 * q], alpha * acc[4 * q + 1], alpha * acc[4 * q + 2], alpha * acc[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int q0 = 0; q0 < KCOLS / 4; q0 += 4) {
+        float4 c[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[q] = c4[q0 + q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = 4 * (q0 + q);
+          c4[q0 + q] = make_float4(fmaf(alpha, acc[j], beta * c[q].x), fmaf(alpha, acc[j + 1], beta * c[q].y),
+                                   fmaf(alpha, acc[j + 2], beta * c[q].z), fmaf(alpha, acc[j + 3], beta * c[q].w));
+        }
+      }
     }
   } else {
-    float4 c[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) c[q] = c4[q];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float4 o;
-      o.x = fmaf(alpha, __uint_as_float(r[4 * q + 0]), beta * c[q].x);
-      o.y = fmaf(alpha, __uint_as_float(r[4 * q + 1]), beta * c[q].y);
-      o.z = fmaf(alpha, __uint_as_float(r[4 * q + 2]), beta * c[q].z);
-      o.w = fmaf(alpha, __uint_as_float(r[4 * q + 3]), beta * c[q].w);
-      c4[q] = o;
-    }
-  }
-}
-
-// Partial tile: row and column predicates; nothing outside m x n is touched.
-__device__ __forceinline__ void epi_partial16(float* __restrict__ crow, const uint32_t (&r)[16], int ncols,
-                                              float alpha, float beta) {
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j < ncols) {
-      const float acc = __uint_as_float(r[j]);
-      crow[j] = (beta == 0.0f) ? alpha * acc : fmaf(alpha, acc, beta * crow[j]);
+    for (int j = 0; j < KCOLS; ++j) {
+      if (j < ncols) crow[j] = (beta == 0.0f) ? alpha * acc[j] : fmaf(alpha, acc[j], beta * crow[j]);
     }
   }
 }
@@ -149,7 +173,7 @@ template <int CG, int BN_CTA, bool SPLIT3>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
   using Cfg = TcCfg<CG, BN_CTA, SPLIT3>;
-  constexpr int RAW = Cfg::kRaw, LO = Cfg::kLo;
+  constexpr int RAW = Cfg::kRaw, LO = Cfg::kLo, KCOLS = Cfg::kCols;
 
   extern __shared__ uint8_t smem_raw_[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw_) + 1023) & ~uintptr_t(1023));
@@ -158,13 +182,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* loA = rawB + RAW * Cfg::kBBytes;
   uint8_t* loB = loA + (SPLIT3 ? LO * Cfg::kABytes : 0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRawBytes + Cfg::kLoBytes);
-  uint64_t* full = bars;                 // [RAW] TMA landed (local)
-  uint64_t* empty_raw = full + RAW;      // [RAW] MMA done with raw stage (commit, multicast)
-  uint64_t* ready = empty_raw + RAW;     // [LO]  split done in all CTAs (leader)
-  uint64_t* empty_lo = ready + LO;       // [LO]  MMA done with lo stage (commit, multicast)
-  uint64_t* tmem_full = empty_lo + LO;   // [2]   accumulator complete (commit, multicast)
-  uint64_t* tmem_empty = tmem_full + 2;  // [2]   epilogue drained accumulator (leader)
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* full = bars;                   // [RAW] TMA landed (local)
+  uint64_t* empty_raw = full + RAW;        // [RAW] MMA done with raw stage (commit, multicast)
+  uint64_t* ready = empty_raw + RAW;       // [LO]  split done in all CTAs (leader)
+  uint64_t* empty_lo = ready + LO;         // [LO]  MMA done with lo stage (commit, multicast)
+  uint64_t* part_full = empty_lo + LO;     // [2]   TMEM partial complete (commit, multicast)
+  uint64_t* part_empty = part_full + 2;    // [2]   partial drained by all promotion warps (leader)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(part_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -182,8 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&empty_lo[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&tmem_full[i], 1);
-      ptx::mbar_init(&tmem_empty[i], 4 * CG);
+      ptx::mbar_init(&part_full[i], 1);
+      ptx::mbar_init(&part_empty[i], kEpiWarps * CG);
     }
     ptx::fence_mbarrier_init();
   }
@@ -198,129 +222,94 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    if (ptx::elect_one()) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-        int tmi, tni;
-        tile_coords(t, p.tiles_m, p.tiles_n, tmi, tni);
-        const int row0 = tmi * Cfg::kTileM + static_cast<int>(rank) * kBMCta;
-        const int col0 = tni * Cfg::kTileN + static_cast<int>(rank) * BN_CTA;
-        for (int kb = 0; kb < p.kblocks; ++kb) {
-          ptx::mbar_wait(&empty_raw[s], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[s], Cfg::kABytes + Cfg::kBBytes);
-          ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * kBK, row0);
+  if (warp < 4) {
+    ptx::setmaxnreg_dec<80>();
+    if (warp == 0) {
+      // ---------------------------------------------------------- producer
+      if (ptx::elect_one()) {
+        int s = 0;
+        uint32_t ph = 0;
+        for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+          int tmi, tni;
+          tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, tmi, tni);
+          const int row0 = tmi * Cfg::kTileM + static_cast<int>(rank) * kBMCta;
+          const int col0 = tni * Cfg::kTileN + static_cast<int>(rank) * BN_CTA;
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            ptx::mbar_wait(&empty_raw[s], ph ^ 1);
+            ptx::mbar_arrive_expect_tx(&full[s], Cfg::kABytes + Cfg::kBBytes);
+            ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * kBK, row0);
 #pragma unroll
-          for (int j = 0; j < BN_CTA / 32; ++j)
-            ptx::tma_load_2d(rawB + s * Cfg::kBBytes + j * 4096, &tmB, &full[s], col0 + 32 * j, kb * kBK);
-          if (++s == RAW) { s = 0; ph ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (rank == 0 && ptx::elect_one()) {
-      constexpr uint32_t idesc = ptx::idesc_tf32(Cfg::kMmaM, Cfg::kMmaN, /*A MN-major*/ 0, /*B MN-major*/ 1);
-      const uint32_t rawA_s = ptx::smem_u32(rawA), rawB_s = ptx::smem_u32(rawB);
-      const uint32_t loA_s = ptx::smem_u32(loA), loB_s = ptx::smem_u32(loB);
-      int s = 0, sl = 0, acc = 0;
-      uint32_t ph = 0, phl = 0, acc_ph = 0;
-      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-        ptx::mbar_wait_cluster(&tmem_empty[acc], acc_ph ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * Cfg::kAccCols);
-        for (int kb = 0; kb < p.kblocks; ++kb) {
-          ptx::mbar_wait_cluster(&ready[sl], phl);
-          ptx::tc_fence_after();
-#pragma unroll
-          for (int ks = 0; ks < kBK / 8; ++ks) {
-            // A: K-major SW128, K step of 8 tf32 = 32 B inside the swizzle row.
-            // B: MN-major SW128_BASE32B, K step of 8 rows = 1024 B (two 512-B
-            //    atoms, SBO); 32-column atoms are 4096 B apart (LBO).
-            const uint64_t aH = ptx::sdesc(rawA_s + s * Cfg::kABytes + ks * 32, 16, 1024, ptx::kLayoutSW128);
-            const uint64_t bH = ptx::sdesc(rawB_s + s * Cfg::kBBytes + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
-            const uint32_t first = (kb | ks) != 0;
-            if constexpr (SPLIT3) {
-              const uint64_t aL = ptx::sdesc(loA_s + sl * Cfg::kABytes + ks * 32, 16, 1024, ptx::kLayoutSW128);
-              const uint64_t bL = ptx::sdesc(loB_s + sl * Cfg::kBBytes + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
-              ptx::mma_tf32<CG>(d, aL, bH, idesc, first);
-              ptx::mma_tf32<CG>(d, aH, bL, idesc, 1u);
-              ptx::mma_tf32<CG>(d, aH, bH, idesc, 1u);
-            } else {
-              ptx::mma_tf32<CG>(d, aH, bH, idesc, first);
-            }
+            for (int j = 0; j < BN_CTA / 32; ++j)
+              ptx::tma_load_2d(rawB + s * Cfg::kBBytes + j * 4096, &tmB, &full[s], col0 + 32 * j, kb * kBK);
+            if (++s == RAW) { s = 0; ph ^= 1; }
           }
-          ptx::mma_commit<CG>(&empty_raw[s]);
-          if constexpr (SPLIT3) ptx::mma_commit<CG>(&empty_lo[sl]);
-          if (++s == RAW) { s = 0; ph ^= 1; }
-          if (++sl == LO) { sl = 0; phl ^= 1; }
-        }
-        ptx::mma_commit<CG>(&tmem_full[acc]);
-        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
-      }
-    }
-  } else if (warp >= 4 && warp < 8) {
-    // ------------------------------------------------------------ epilogue
-    const int ew = warp & 3;  // TMEM lane quarter owned by this warp
-    int acc = 0;
-    uint32_t acc_ph = 0;
-    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-      int tmi, tni;
-      tile_coords(t, p.tiles_m, p.tiles_n, tmi, tni);
-      ptx::mbar_wait(&tmem_full[acc], acc_ph);
-      ptx::tc_fence_after();
-      const int cta_row0 = tmi * Cfg::kTileM + static_cast<int>(rank) * kBMCta;
-      const int col0 = tni * Cfg::kTileN;
-      const int row = cta_row0 + ew * 32 + lane;
-      const bool full_tile = (cta_row0 + kBMCta <= p.m) && (col0 + Cfg::kTileN <= p.n);
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * Cfg::kAccCols);
-      float* crow = p.C + static_cast<long long>(row) * p.ldc + col0;
-#pragma unroll 1
-      for (int c = 0; c < Cfg::kTileN / 16; ++c) {
-        uint32_t r[16];
-        ptx::tmem_ld_32x32b_x16(taddr + c * 16, r);
-        ptx::tmem_ld_wait();
-        if (full_tile) {
-          epi_full16(crow + c * 16, r, p.alpha, p.beta);
-        } else if (row < p.m) {
-          const int ncols = p.n - (col0 + c * 16);
-          if (ncols > 0) epi_partial16(crow + c * 16, r, ncols, p.alpha, p.beta);
         }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) ptx::mbar_arrive_cluster(&tmem_empty[acc], 0);
-        else ptx::mbar_arrive(&tmem_empty[acc]);
+    } else if (warp == 1) {
+      // ---------------------------------------------------------- MMA issuer
+      if (rank == 0 && ptx::elect_one()) {
+        constexpr uint32_t idesc = ptx::idesc_tf32(Cfg::kMmaM, Cfg::kMmaN, /*A MN-major*/ 0, /*B MN-major*/ 1);
+        const uint32_t rawA_s = ptx::smem_u32(rawA), rawB_s = ptx::smem_u32(rawB);
+        const uint32_t loA_s = ptx::smem_u32(loA), loB_s = ptx::smem_u32(loB);
+        int s = 0, sl = 0, pb = 0;
+        uint32_t ph = 0, phl = 0, pph = 0;
+        for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+          for (int kb0 = 0; kb0 < p.kblocks; kb0 += p.kc_blocks) {
+            const int kb1 = min(kb0 + p.kc_blocks, p.kblocks);
+            ptx::mbar_wait_cluster(&part_empty[pb], pph ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem_base + static_cast<uint32_t>(pb * Cfg::kMmaN);
+            for (int kb = kb0; kb < kb1; ++kb) {
+              ptx::mbar_wait_cluster(&ready[sl], phl);
+              ptx::tc_fence_after();
+#pragma unroll
+              for (int ks = 0; ks < kBK / 8; ++ks) {
+                // A: K-major SW128, K step of 8 tf32 = 32 B inside the swizzle row.
+                // B: MN-major SW128_BASE32B, K step of 8 rows = 1024 B (two 512-B
+                //    atoms, SBO); 32-column atoms are 4096 B apart (LBO).
+                const uint64_t aH = ptx::sdesc(rawA_s + s * Cfg::kABytes + ks * 32, 16, 1024, ptx::kLayoutSW128);
+                const uint64_t bH =
+                    ptx::sdesc(rawB_s + s * Cfg::kBBytes + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
+                const uint32_t acc = (kb != kb0 || ks != 0) ? 1u : 0u;  // fresh partial per K_c chunk
+                if constexpr (SPLIT3) {
+                  const uint64_t aL = ptx::sdesc(loA_s + sl * Cfg::kABytes + ks * 32, 16, 1024, ptx::kLayoutSW128);
+                  const uint64_t bL =
+                      ptx::sdesc(loB_s + sl * Cfg::kBBytes + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
+                  ptx::mma_tf32<CG>(d, aL, bH, idesc, acc);
+                  ptx::mma_tf32<CG>(d, aH, bL, idesc, 1u);
+                  ptx::mma_tf32<CG>(d, aH, bH, idesc, 1u);
+                } else {
+                  ptx::mma_tf32<CG>(d, aH, bH, idesc, acc);
+                }
+              }
+              ptx::mma_commit<CG>(&empty_raw[s]);
+              ptx::mma_commit<CG>(&empty_lo[sl]);  // also paces the ready ring when !SPLIT3
+              if (++s == RAW) { s = 0; ph ^= 1; }
+              if (++sl == LO) { sl = 0; phl ^= 1; }
+            }
+            ptx::mma_commit<CG>(&part_full[pb]);
+            if (++pb == 2) { pb = 0; pph ^= 1; }
+          }
+        }
       }
-      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
-  } else if (warp >= 8) {
+  } else if (warp < 8) {
     // ------------------------------------------------------------ split
-    const int st = threadIdx.x - 256;
+    ptx::setmaxnreg_dec<80>();
+    const int st = threadIdx.x - 128;
+    const uint32_t rawA_s = ptx::smem_u32(rawA), rawB_s = ptx::smem_u32(rawB);
+    const uint32_t loA_s = ptx::smem_u32(loA), loB_s = ptx::smem_u32(loB);
     int s = 0, sl = 0;
     uint32_t ph = 0, phl = 0;
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
       for (int kb = 0; kb < p.kblocks; ++kb) {
         ptx::mbar_wait(&full[s], ph);
+        // The ready ring must not run more than LO stages ahead of the MMA
+        // (an mbarrier phase may not complete twice before it is observed).
+        ptx::mbar_wait(&empty_lo[sl], phl ^ 1);
         if constexpr (SPLIT3) {
-          ptx::mbar_wait(&empty_lo[sl], phl ^ 1);
-          const uint4* srcA = reinterpret_cast<const uint4*>(rawA + s * Cfg::kABytes);
-          uint4* dstA = reinterpret_cast<uint4*>(loA + sl * Cfg::kABytes);
-#pragma unroll
-          for (int i = 0; i < Cfg::kABytes / 16 / kSplitThreads; ++i) {
-            const uint4 v = srcA[i * kSplitThreads + st];
-            dstA[i * kSplitThreads + st] = make_uint4(tf32_lo_bits(v.x), tf32_lo_bits(v.y), tf32_lo_bits(v.z), tf32_lo_bits(v.w));
-          }
-          const uint4* srcB = reinterpret_cast<const uint4*>(rawB + s * Cfg::kBBytes);
-          uint4* dstB = reinterpret_cast<uint4*>(loB + sl * Cfg::kBBytes);
-#pragma unroll
-          for (int i = 0; i < Cfg::kBBytes / 16 / kSplitThreads; ++i) {
-            const uint4 v = srcB[i * kSplitThreads + st];
-            dstB[i * kSplitThreads + st] = make_uint4(tf32_lo_bits(v.x), tf32_lo_bits(v.y), tf32_lo_bits(v.z), tf32_lo_bits(v.w));
-          }
+          split_tile<Cfg::kABytes>(rawA_s + s * Cfg::kABytes, loA_s + sl * Cfg::kABytes, st);
+          split_tile<Cfg::kBBytes>(rawB_s + s * Cfg::kBBytes, loB_s + sl * Cfg::kBBytes, st);
           ptx::fence_proxy_async_smem();
         }
         __syncwarp();
@@ -330,6 +319,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (++s == RAW) { s = 0; ph ^= 1; }
         if (++sl == LO) { sl = 0; phl ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ promotion + epilogue
+    ptx::setmaxnreg_inc<176>();
+    const int q = warp & 3;             // TMEM lane quarter (rows 32q..32q+31 of this CTA)
+    const int h = (warp - 8) >> 2;      // column half
+    int pb = 0;
+    uint32_t pph = 0;
+    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+      int tmi, tni;
+      tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, tmi, tni);
+      float acc[KCOLS];
+#pragma unroll
+      for (int j = 0; j < KCOLS; ++j) acc[j] = 0.0f;
+      for (int kb0 = 0; kb0 < p.kblocks; kb0 += p.kc_blocks) {
+        ptx::mbar_wait(&part_full[pb], pph);
+        ptx::tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                               static_cast<uint32_t>(pb * Cfg::kMmaN + h * KCOLS);
+#pragma unroll
+        for (int c = 0; c < KCOLS; c += 16) {
+          uint32_t r[16];
+          ptx::tmem_ld_32x32b_x16(taddr + c, r);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(r[j]);  // RN promotion
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster(&part_empty[pb], 0);
+          else ptx::mbar_arrive(&part_empty[pb]);
+        }
+        if (++pb == 2) { pb = 0; pph ^= 1; }
+      }
+      const int row = tmi * Cfg::kTileM + static_cast<int>(rank) * kBMCta + q * 32 + lane;
+      const int col0 = tni * Cfg::kTileN + h * KCOLS;
+      if (row < p.m && col0 < p.n) {
+        const bool full_row = (col0 + KCOLS <= p.n);
+        epi_store<KCOLS>(p.C + static_cast<long long>(row) * p.ldc + col0, acc, full_row, p.n - col0, p.alpha,
+                         p.beta);
       }
     }
   }
@@ -403,6 +434,10 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t stream) {
   p.tiles_n = static_cast<int>((a.n + Cfg::kTileN - 1) / Cfg::kTileN);
   p.num_tiles = p.tiles_m * p.tiles_n;
   p.kblocks = static_cast<int>((a.k + kBK - 1) / kBK);
+  p.kc_blocks = kKcBlocksDefault;
+  p.group_m = kGroupMDefault;
+  if (const char* e = std::getenv("TM_KC_BLOCKS")) p.kc_blocks = std::max(1, std::atoi(e));  // tuning knob
+  if (const char* e = std::getenv("TM_GROUP_M")) p.group_m = std::max(1, std::atoi(e));     // tuning knob
   p.alpha = a.alpha;
   p.beta = a.beta;
   p.C = a.C;

@@ -164,3 +164,23 @@ def test_c3b_8192_sampled_rows():
     C, _ = run(A, B, C0, si.ALPHA, si.BETA, AUTO)
     rows = si.sample_rows(m, count=64, tile=256)
     assert max_err(C, A, B, C0, si.ALPHA, si.BETA, rows=rows) <= TOL
+
+
+@pytest.mark.parametrize("cfg,kind", [("C3b", "positive"), ("C5", "uniform"), ("C5", "positive")])
+def test_large_k_accuracy_sampled_rows(cfg, kind):
+    """Full-size configs (BASELINE.json configs[4] = C5, the bench workload)
+    in the launch configuration bench.py times (AUTO path).  All-positive
+    inputs stress the tensor core's round-toward-zero accumulation; K_c
+    promotion keeps them inside the bar too."""
+    import torch
+    import paper_1804_10694_b200 as tm
+    m, n, k = si.CONFIGS[cfg]
+    A, B, C0 = si.matrices(m, n, k, si.SEEDS[cfg], kind=kind)
+    dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C0))
+    tm.sgemm(dA, dB, dC, si.ALPHA, si.BETA)
+    torch.cuda.synchronize()
+    rows = si.sample_rows(m, count=40, tile=256)
+    C = dC[torch.from_numpy(rows).cuda()].cpu().numpy()
+    del dA, dB, dC
+    R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0, rows=rows)
+    assert float(np.max(oracle.normalized_error(C, R, D))) <= TOL
