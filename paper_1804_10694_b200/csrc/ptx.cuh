@@ -74,10 +74,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Arrive on the barrier at the same smem offset in CTA `rank` (cluster scope).
+// Arrive on the barrier at the same smem offset in CTA `rank` of the cluster.
+// Default (CTA-scope release) semantics: the data this arrive publishes lives
+// in the arriving CTA's own shared memory / TMEM (already made visible to the
+// async proxy by the caller's fence), so no GPU-scope MEMBAR is needed; the
+// .release.cluster form costs a MEMBAR.ALL.GPU per arrive (measured: it made
+// the split warps the pipeline bottleneck).
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
   uint32_t remote = mapa(smem_u32(bar), rank);
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
