@@ -158,6 +158,20 @@ tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float a
                         const float* A_local, int64_t lda, float* B, int64_t ldb, int root,
                         float beta, float* C_local, int64_t ldc, void* stream);
 
+/* Single-process loopback of tm_sgemm_dist (verification mode, DESIGN.md
+ * section 10): emulates `nranks` ranks one after another on the CURRENT device
+ * with the identical partition, K-chunk schedule and beta chain; each chunk
+ * "broadcast" is a device-to-device copy from Bs[root] into Bs[r].
+ *   A_locals[r], Bs[r], C_locals[r]: device pointers (host arrays of nranks),
+ *   shaped as tm_sgemm_dist's A_local, B, C_local for rank r.
+ *   bytes_received: optional host array of nranks counters (bytes each rank's
+ *   B received), or NULL.
+ * Synchronises `stream`; errors as tm_sgemm_dist. */
+tm_status tm_sgemm_dist_loopback(int nranks, int root, int64_t m, int64_t n, int64_t k, float alpha,
+                                 const float* const* A_locals, int64_t lda, float* const* Bs, int64_t ldb,
+                                 float beta, float* const* C_locals, int64_t ldc, uint64_t* bytes_received,
+                                 void* stream);
+
 /* Variant: B is pre-sharded by k-rows (B_shard = rows [k0, k0+kr) of B from
  * tm_dist_rows(k, ...), leading dimension ldb), all-gathered into the
  * caller-owned B_full (k x n, ldb).  Requires every rank's shard to have the

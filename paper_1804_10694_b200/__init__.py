@@ -27,7 +27,7 @@ lib_path = os.path.join(_PKG, "_lib", "libtm.so")
 EXPORTED_SYMBOLS = [
     "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
     "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
-    "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_allgather", "tm_comm_bytes_received",
+    "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_bytes_received",
 ]
 
 
@@ -60,6 +60,7 @@ def _load():
     L.tm_comm_rank.argtypes = [vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
     L.tm_comm_bytes_received.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
     L.tm_sgemm_dist.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, i64, ci, f32, vp, i64, vp]
+    L.tm_sgemm_dist_loopback.argtypes = [ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, vp]
     L.tm_sgemm_dist_allgather.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, vp, i64, f32, vp, i64, vp]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(L, name)
@@ -188,6 +189,21 @@ def dist_chunks(k: int, nranks: int):
         _check(lib.tm_dist_chunk(k, nranks, i, ctypes.byref(a), ctypes.byref(b)), "tm_dist_chunk")
         out.append((a.value, b.value))
     return out
+
+
+def sgemm_dist_loopback(m, n, k, A_locals, Bs, C_locals, alpha=1.0, beta=0.0, root=0, stream=None):
+    """Single-process emulation of the row-sharded mode:
+    len(A_locals) simulated ranks on the current GPU, same schedule as
+    Comm.sgemm.  Returns the bytes each simulated rank received."""
+    P = len(A_locals)
+    arr = lambda ts: (ctypes.c_void_p * P)(*[t.data_ptr() for t in ts])
+    lda = next((_ld(a) for a in A_locals if a.shape[0] > 0), max(k, 1))
+    ldc = next((_ld(c) for c in C_locals if c.shape[0] > 0), max(n, 1))
+    got = (ctypes.c_uint64 * P)()
+    st = lib.tm_sgemm_dist_loopback(P, int(root), m, n, k, float(alpha), arr(A_locals), lda, arr(Bs), _ld(Bs[0]),
+                                    float(beta), arr(C_locals), ldc, got, _stream(stream))
+    _check(st, "tm_sgemm_dist_loopback")
+    return [int(x) for x in got]
 
 
 def unique_id() -> bytes:

@@ -171,40 +171,46 @@ tm_status tm_dist_chunk(int64_t k, int nranks, int idx, int64_t* k0, int64_t* kr
   return TM_OK;
 }
 
-tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha, const float* A_local,
-                        int64_t lda, float* B, int64_t ldb, int root, float beta, float* C_local, int64_t ldc,
-                        void* stream_) {
-  if (!comm || root < 0 || root >= comm->nranks || m < 0 || n < 0 || k < 0) return TM_ERR_INVALID_VALUE;
+}  // extern "C"
+
+namespace {
+
+// The per-rank schedule of the row-sharded GEMM, shared by the NCCL mode and
+// the single-process loopback mode.  `xfer(p, count)` enqueues the transfer of
+// `count` floats of B at `p` from the root on `comm_stream` (ncclBroadcast, or
+// a device copy in loopback); the GEMM of chunk c waits only for chunk c.
+template <class Xfer>
+tm_status dist_schedule(int nranks, int rank, int root, int64_t m, int64_t n, int64_t k, float alpha,
+                        const float* A_local, int64_t lda, float* B, int64_t ldb, float beta, float* C_local,
+                        int64_t ldc, cudaStream_t stream, cudaStream_t comm_stream, cudaEvent_t ev_start,
+                        cudaEvent_t* ev_chunk, uint64_t* bytes_received, Xfer&& xfer) {
   int64_t row0 = 0, rows = 0;
-  tm_dist_rows(m, comm->nranks, comm->rank, &row0, &rows);
-  (void)row0;
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  tm_dist_rows(m, nranks, rank, &row0, &rows);
   const bool reads_ab = alpha != 0.0f && k > 0 && n > 0;
-  if (!reads_ab || comm->nranks == 1) {
+  if (!reads_ab || nranks == 1) {
     // Nothing to exchange (P == 1, or B is not read): exactly tm_sgemm.
     return tm_sgemm(rows, n, k, alpha, A_local, lda, B, ldb, beta, C_local, ldc, stream);
   }
   if (!B || ldb < (n > 1 ? n : 1)) return TM_ERR_INVALID_VALUE;
   int64_t nchunks = 0, kc = 0;
-  tm_dist_chunk(k, comm->nranks, -1, &nchunks, &kc);
+  tm_dist_chunk(k, nranks, -1, &nchunks, &kc);
   if (nchunks > kMaxChunks) return TM_ERR_INTERNAL;
-  if (cudaEventRecord(comm->ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
-  if (cudaStreamWaitEvent(comm->stream, comm->ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
+  if (cudaEventRecord(ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (cudaStreamWaitEvent(comm_stream, ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
   int used = 0;
   for (int64_t k0 = 0; k0 < k; k0 += kc, ++used) {
     const int64_t kr = (k0 + kc <= k) ? kc : k - k0;
     // Root sends in place; the last row's padding beyond n is inside k*ldb.
     const size_t count = static_cast<size_t>(kr) * static_cast<size_t>(ldb);
-    float* p = B + k0 * ldb;
-    if (g_nccl.Broadcast(p, p, count, ncclFloat32, root, comm->comm, comm->stream) != ncclSuccess)
-      return TM_ERR_NCCL;
-    if (comm->rank != root) comm->bytes_received += count * 4;
-    if (cudaEventRecord(comm->ev_chunk[used], comm->stream) != cudaSuccess) return TM_ERR_CUDA;
+    tm_status st = xfer(B + k0 * ldb, count);
+    if (st != TM_OK) return st;
+    if (rank != root && bytes_received) *bytes_received += count * 4;
+    if (cudaEventRecord(ev_chunk[used], comm_stream) != cudaSuccess) return TM_ERR_CUDA;
   }
   used = 0;
   for (int64_t k0 = 0; k0 < k; k0 += kc, ++used) {
     const int64_t kr = (k0 + kc <= k) ? kc : k - k0;
-    if (cudaStreamWaitEvent(stream, comm->ev_chunk[used], 0) != cudaSuccess) return TM_ERR_CUDA;
+    if (cudaStreamWaitEvent(stream, ev_chunk[used], 0) != cudaSuccess) return TM_ERR_CUDA;
     if (rows > 0) {
       tm_status st = tm_sgemm(rows, n, kr, alpha, A_local + k0, lda, B + k0 * ldb, ldb, k0 == 0 ? beta : 1.0f,
                               C_local, ldc, stream);
@@ -212,6 +218,61 @@ tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float a
     }
   }
   return TM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha, const float* A_local,
+                        int64_t lda, float* B, int64_t ldb, int root, float beta, float* C_local, int64_t ldc,
+                        void* stream_) {
+  if (!comm || root < 0 || root >= comm->nranks || m < 0 || n < 0 || k < 0) return TM_ERR_INVALID_VALUE;
+  auto xfer = [&](float* p, size_t count) -> tm_status {
+    return g_nccl.Broadcast(p, p, count, ncclFloat32, root, comm->comm, comm->stream) == ncclSuccess ? TM_OK
+                                                                                                    : TM_ERR_NCCL;
+  };
+  return dist_schedule(comm->nranks, comm->rank, root, m, n, k, alpha, A_local, lda, B, ldb, beta, C_local, ldc,
+                       static_cast<cudaStream_t>(stream_), comm->stream, comm->ev_start, comm->ev_chunk,
+                       &comm->bytes_received, xfer);
+}
+
+tm_status tm_sgemm_dist_loopback(int nranks, int root, int64_t m, int64_t n, int64_t k, float alpha,
+                                 const float* const* A_locals, int64_t lda, float* const* Bs, int64_t ldb,
+                                 float beta, float* const* C_locals, int64_t ldc, uint64_t* bytes_received,
+                                 void* stream_) {
+  if (nranks < 1 || root < 0 || root >= nranks || !A_locals || !Bs || !C_locals || m < 0 || n < 0 || k < 0)
+    return TM_ERR_INVALID_VALUE;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_chunk[kMaxChunks] = {};
+  tm_status st = TM_OK;
+  bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) == cudaSuccess;
+  for (int i = 0; ok && i < kMaxChunks; ++i)
+    ok = cudaEventCreateWithFlags(&ev_chunk[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) st = TM_ERR_CUDA;
+  if (bytes_received)
+    for (int r = 0; r < nranks; ++r) bytes_received[r] = 0;
+  // Ranks run one after another on this device; rank r's "broadcast" copies
+  // the root's chunk into rank r's B (the root's own transfer is a no-op).
+  for (int r = 0; st == TM_OK && r < nranks; ++r) {
+    const float* root_B = Bs[root];
+    auto xfer = [&](float* p, size_t count) -> tm_status {
+      if (r == root) return TM_OK;
+      const float* src = root_B + (p - Bs[r]);
+      return cudaMemcpyAsync(p, src, count * 4, cudaMemcpyDeviceToDevice, cs) == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+    };
+    st = dist_schedule(nranks, r, root, m, n, k, alpha, A_locals[r], lda, Bs[r], ldb, beta, C_locals[r], ldc, stream,
+                       cs, ev_start, ev_chunk, bytes_received ? &bytes_received[r] : nullptr, xfer);
+    if (st == TM_OK && cudaStreamSynchronize(stream) != cudaSuccess) st = TM_ERR_CUDA;
+  }
+  if (cs) cudaStreamSynchronize(cs);
+  for (int i = 0; i < kMaxChunks; ++i)
+    if (ev_chunk[i]) cudaEventDestroy(ev_chunk[i]);
+  if (ev_start) cudaEventDestroy(ev_start);
+  if (cs) cudaStreamDestroy(cs);
+  return st;
 }
 
 tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha,

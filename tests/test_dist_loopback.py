@@ -1,0 +1,100 @@
+"""Row-sharded multi-GPU mode, verified on one GPU through the loopback
+(tm_sgemm_dist_loopback): the same partition, K-chunk schedule and beta chain
+as tm_sgemm_dist, with each chunk broadcast replaced by a device copy.
+
+Checks (SURVEY.md section 4 "Distribution semantics"): each rank's shard equals
+the oracle's rows (rows distributed; no gather);
+uneven m % P; P = 1 is bit-identical to tm_sgemm; root != 0; each non-root rank
+receives exactly k*ldb*4 bytes (message conservation)."""
+import numpy as np
+import pytest
+
+import oracle
+import seeded_inputs as si
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def _run(P, root, m, n, k, seed, kind="uniform", ldb=None):
+    import torch
+    import paper_1804_10694_b200 as tm
+    ldb = n if ldb is None else ldb
+    A, B, C0 = si.matrices(m, n, k, seed, kind=kind, ldb=ldb)
+    dA = torch.from_numpy(np.ascontiguousarray(A)).cuda()
+    Bfull = np.full((k, ldb), np.nan, dtype=np.float32)
+    Bfull[:, :n] = B
+    Bs, As, Cs, parts = [], [], [], []
+    for r in range(P):
+        r0, rows = tm.dist_rows(m, P, r)
+        parts.append((r0, rows))
+        As.append(dA[r0:r0 + rows])
+        Cs.append(torch.from_numpy(np.ascontiguousarray(C0[r0:r0 + rows])).cuda())
+        if r == root:
+            Bs.append(torch.from_numpy(Bfull).cuda())
+        else:
+            Bs.append(torch.full((k, ldb), float("nan"), dtype=torch.float32, device="cuda"))
+    got = tm.sgemm_dist_loopback(m, n, k, As, [b for b in Bs], Cs, si.ALPHA, si.BETA, root=root)
+    torch.cuda.synchronize()
+    return A, B, C0, parts, [c.cpu().numpy() for c in Cs], got, [b[:, :n].cpu().numpy() for b in Bs]
+
+
+@pytest.mark.parametrize("P,root", [(2, 0), (3, 1), (8, 0), (8, 5)])
+def test_loopback_shards_match_oracle(P, root):
+    m, n, k = 1060, 260, 1100   # uneven rows; two K-chunks of 576 and 524
+    A, B, C0, parts, Cs, got, Bs = _run(P, root, m, n, k, seed=40 + P)
+    R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0)
+    for r, ((r0, rows), C) in enumerate(zip(parts, Cs)):
+        assert C.shape == (rows, n)
+        if rows:
+            e = float(np.max(oracle.normalized_error(C, R[r0:r0 + rows], D[r0:r0 + rows])))
+            assert e <= TOL, (r, e)
+        assert np.array_equal(Bs[r], B)  # every rank ends with root's B
+        assert got[r] == (0 if r == root else k * n * 4)  # message conservation
+
+
+def test_loopback_p1_bit_identical_to_sgemm():
+    import torch
+    import paper_1804_10694_b200 as tm
+    m, n, k = 700, 300, 900
+    A, B, C0, parts, Cs, got, _ = _run(1, 0, m, n, k, seed=50)
+    dA, dB, dC = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (A, B, C0))
+    tm.sgemm(dA, dB, dC, si.ALPHA, si.BETA)
+    assert np.array_equal(Cs[0], dC.cpu().numpy()) and got == [0]
+
+
+def test_loopback_more_ranks_than_rows():
+    m, n, k = 5, 40, 700
+    A, B, C0, parts, Cs, got, _ = _run(8, 0, m, n, k, seed=51)
+    R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0)
+    assert sum(rows for _, rows in parts) == m
+    for (r0, rows), C in zip(parts, Cs):
+        if rows:
+            assert float(np.max(oracle.normalized_error(C, R[r0:r0 + rows], D[r0:r0 + rows]))) <= TOL
+
+
+def test_loopback_c5_p8_sampled_rows():
+    """BASELINE.json configs[4]: 16384^3 row-sharded over 8 ranks (8 chunks of
+    2048), sampled rows incl. every shard boundary, all-positive stress data
+    (the beta chain adds 7 extra fp32 roundings per element)."""
+    import torch
+    import paper_1804_10694_b200 as tm
+    m = n = k = 16384
+    P = 8
+    A, B, C0 = si.matrices(m, n, k, si.SEEDS["C5"], kind="positive")
+    dA = torch.from_numpy(A).cuda()
+    dB = torch.from_numpy(B).cuda()
+    Bs = [dB] + [torch.empty_like(dB) for _ in range(P - 1)]
+    As, Cs, bounds = [], [], []
+    for r in range(P):
+        r0, rows = tm.dist_rows(m, P, r)
+        bounds += [r0, r0 + rows - 1]
+        As.append(dA[r0:r0 + rows])
+        Cs.append(torch.from_numpy(C0[r0:r0 + rows].copy()).cuda())
+    tm.sgemm_dist_loopback(m, n, k, As, Bs, Cs, si.ALPHA, si.BETA)
+    C = torch.cat(Cs).cpu().numpy()
+    del Bs, dA, dB, As, Cs
+    torch.cuda.empty_cache()
+    rows = si.sample_rows(m, count=24, tile=2048, extra=bounds)
+    R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0, rows=rows)
+    assert float(np.max(oracle.normalized_error(C[rows], R, D))) <= TOL
