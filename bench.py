@@ -238,7 +238,10 @@ def main():
     comm = tm.Comm(rank, world) if world > 1 else None
     in_bytes = 4 * (m * k + k * n + m * n)
     small = in_bytes < 2 * 126 * 2 ** 20  # inputs fit in L2: flush between iterations
-    flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda") if small else None
+    # L2 flush by READING 512 MiB (a write-flush would leave ~126 MB of dirty
+    # lines whose write-back competes with the next GEMM's DRAM reads)
+    flush = torch.ones(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda") if small else None
+    flush_out = torch.empty(1, dtype=torch.float32, device="cuda")
 
     def step():
         if comm is None:
@@ -264,7 +267,7 @@ def main():
         t_start.record(stream)
         for i in range(args.steps):
             if flush is not None:
-                flush.zero_()
+                torch.sum(flush, dim=0, out=flush_out[0])
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
@@ -310,7 +313,7 @@ def main():
         if kernel != "simt" else "f32", "data": "synthetic (seeded U[-1,1) fp32, device-generated)",
         "config": {"workload": desc, "m": m, "n": n, "k": k, "alpha": alpha, "beta": beta, "path": path,
                    "rows_per_rank": rows, "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2, no flush" if not small else "L2 flushed (512 MiB write) between steps"},
+                   "l2": "inputs larger than L2, no flush" if not small else "L2 flushed (512 MiB read) between steps"},
         "roofline": roof, "gpu_launches": launches, "clocks": clocks.summary(),
     }
 

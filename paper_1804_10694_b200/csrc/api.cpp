@@ -6,7 +6,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "tm_internal.h"
 
@@ -66,7 +68,7 @@ enum class Path { kInvalid, kNoop, kScale, kTc, kSimt };
 
 struct Plan {
   Path path = Path::kInvalid;
-  TcChoice tc{2, 128, true};
+  TcChoice tc{2, 128, true, false};
 };
 
 bool tc_aligned(const GemmArgs& a) {
@@ -111,12 +113,15 @@ Plan make_plan(const GemmArgs& a, int algo, int num_sms) {
   if (pl.path == Path::kTc) {
     pl.tc = plan_tc(a.m, a.n, a.k, num_sms > 0 ? num_sms : 148);
     pl.tc.split3 = (algo != TM_ALGO_TF32X1);
-    const char* force = std::getenv("TM_TC_CONFIG");  // "cg,bn" -- tests/bench only
+    const char* force = std::getenv("TM_TC_CONFIG");  // "cg,bn[,sk]" -- tests/bench only
     if (force) {
-      int cg = 0, bn = 0;
-      if (std::sscanf(force, "%d,%d", &cg, &bn) == 2 && (cg == 1 || cg == 2) && (bn == 32 || bn == 64 || bn == 128)) {
+      int cg = 0, bn = 0, sk = -1;
+      const int got = std::sscanf(force, "%d,%d,%d", &cg, &bn, &sk);
+      if (got >= 2 && (cg == 1 || cg == 2) && (bn == 32 || bn == 64 || bn == 128)) {
         pl.tc.cg = cg;
         pl.tc.bn_cta = bn;
+        pl.tc.streamk = plan_streamk(a.m, a.n, a.k, cg, bn, num_sms > 0 ? num_sms : 148);
+        if (got == 3 && (sk == 0 || sk == 1)) pl.tc.streamk = sk == 1;
       }
     }
   }
@@ -137,6 +142,7 @@ tm_status run(const GemmArgs& a, int algo, cudaStream_t stream) {
                  static_cast<long long>(a.m), static_cast<long long>(a.n), static_cast<long long>(a.k), algo,
                  pl.path == Path::kTc ? "tf32x3" : pl.path == Path::kSimt ? "simt" : "scale", pl.tc.cg,
                  pl.tc.bn_cta, pl.tc.split3 ? 1 : 0);
+  if (log_enabled() && pl.path == Path::kTc) std::fprintf(stderr, "[tm]   streamk=%d\n", pl.tc.streamk ? 1 : 0);
   switch (pl.path) {
     case Path::kScale:
       return launch_scale(a.m, a.n, a.beta, a.C, a.ldc, stream);
@@ -186,7 +192,57 @@ tm_status ws_get(int dev, size_t bytes, Workspace** out) {
   return TM_OK;
 }
 
+// ------------------------------------------------------------ stream-K workspace
+struct SkWorkspace {
+  float* ws = nullptr;
+  size_t ws_bytes = 0;
+  unsigned* flags = nullptr;
+  size_t flag_count = 0;
+  unsigned epoch = 0;
+};
+std::mutex g_sk_mu;
+std::map<std::pair<int, cudaStream_t>, SkWorkspace> g_sk;
+
 }  // namespace
+
+tm_status streamk_workspace(cudaStream_t stream, size_t ws_bytes, size_t flag_count, float** ws, unsigned** flags,
+                            unsigned* epoch) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TM_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(g_sk_mu);
+  SkWorkspace& w = g_sk[{dev, stream}];
+  if (w.ws_bytes < ws_bytes) {
+    if (w.ws) cudaFree(w.ws);
+    w.ws = nullptr;
+    w.ws_bytes = 0;
+    if (cudaMalloc(&w.ws, ws_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return TM_ERR_OUT_OF_MEMORY;
+    }
+    w.ws_bytes = ws_bytes;
+  }
+  if (w.flag_count < flag_count) {
+    if (w.flags) cudaFree(w.flags);
+    w.flags = nullptr;
+    w.flag_count = 0;
+    if (cudaMalloc(&w.flags, flag_count * sizeof(unsigned)) != cudaSuccess) {
+      cudaGetLastError();
+      return TM_ERR_OUT_OF_MEMORY;
+    }
+    if (cudaMemsetAsync(w.flags, 0, flag_count * sizeof(unsigned), stream) != cudaSuccess) return TM_ERR_CUDA;
+    w.flag_count = flag_count;
+    w.epoch = 0;
+  }
+  if (++w.epoch == 0) {  // wrapped: flags could hold any old epoch; clear them
+    if (cudaMemsetAsync(w.flags, 0, w.flag_count * sizeof(unsigned), stream) != cudaSuccess) return TM_ERR_CUDA;
+    w.epoch = 1;
+  }
+  *ws = w.ws;
+  *flags = w.flags;
+  *epoch = w.epoch;
+  return TM_OK;
+}
+
 }  // namespace tmk
 
 using tmk::GemmArgs;

@@ -10,15 +10,30 @@
 //   efficiency: 1-CTA tiles read both operands from one SM's shared memory
 //               (about 1.5x the smem bytes per MMA of a CTA pair), and narrow
 //               tiles pay fixed per-stage costs -- measured factors, DESIGN.md.
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 
 #include "tm_internal.h"
 
 namespace tmk {
 
+// Stream-K pays off when the data-parallel schedule leaves a partial last
+// wave that matters: fewer than 8 waves, tiles not a multiple of the cluster
+// count, and at least 2 K-blocks of work per cluster.
+bool plan_streamk(int64_t m, int64_t n, int64_t k, int cg, int bn_cta, int num_sms) {
+  const int64_t tile_m = 128LL * cg, tile_n = static_cast<int64_t>(bn_cta) * cg;
+  const int64_t tiles = ((m + tile_m - 1) / tile_m) * ((n + tile_n - 1) / tile_n);
+  const int64_t units = num_sms / cg;
+  const int64_t kb = (k + 31) / 32;
+  if (tiles % units == 0) return false;
+  if (tiles >= 8 * units) return false;
+  return tiles * kb >= 2 * units;
+}
+
 TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms) {
-  static const TcChoice cands[] = {{2, 128, true}, {2, 64, true}, {2, 32, true},
-                                   {1, 128, true}, {1, 64, true}, {1, 32, true}};
+  static const TcChoice cands[] = {{2, 128, true, false}, {2, 64, true, false}, {2, 32, true, false},
+                                   {1, 128, true, false}, {1, 64, true, false}, {1, 32, true, false}};
   TcChoice best = cands[0];
   double best_t = 1e300;
   const int64_t kb = (k + 31) / 32;
@@ -27,18 +42,31 @@ TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms) {
     const int64_t tiles = ((m + tile_m - 1) / tile_m) * ((n + tile_n - 1) / tile_n);
     const int64_t units = num_sms / c.cg;
     const int64_t waves = (tiles + units - 1) / units;
-    double per_tile = static_cast<double>(kb) * 4.0 * 3.0 * (c.cg * c.bn_cta / 2.0) + 2000.0;  // + fill/epilogue
+    const bool sk = plan_streamk(m, n, k, c.cg, c.bn_cta, num_sms);
+    const double kb_cycles = 4.0 * 3.0 * (c.cg * c.bn_cta / 2.0);
+    // + fixed per-tile cost: pipeline fill and the epilogue (about 5 us, ~10k
+    // cycles, measured with TM_TRACE_PATH), scaled by the tile's column count
+    const double epi = 4000.0 + 6000.0 * (c.cg * c.bn_cta) / 256.0;
+    double per_tile = static_cast<double>(kb) * kb_cycles + epi;
     // Sustained MMA efficiency per configuration, measured on B200 at 8192^3
     // (DESIGN.md "Planner"): narrower tiles re-read A from shared memory more
     // often per MMA and a 1-CTA tile reads all of B from one SM.
     double eff = 1.0;
-    if (c.cg == 2) eff = (c.bn_cta == 128) ? 1.0 : (c.bn_cta == 64) ? 0.6 : 0.35;
-    else eff = (c.bn_cta == 128) ? 0.75 : (c.bn_cta == 64) ? 0.45 : 0.25;
+    if (c.cg == 2) eff = (c.bn_cta == 128) ? 1.0 : (c.bn_cta == 64) ? 0.88 : 0.58;
+    else eff = (c.bn_cta == 128) ? 0.79 : (c.bn_cta == 64) ? 0.49 : 0.3;
     // Wasted MMA work on zero-filled tile padding is already in `waves`.
-    const double t = static_cast<double>(waves) * per_tile / eff;
+    double t = static_cast<double>(waves) * per_tile / eff;
+    if (sk) {  // balanced iterations + one fixed-order reduction per cluster
+      const double iters = static_cast<double>(tiles) * static_cast<double>(kb);
+      // + one serial fixed-order reduction per tile over ~units/tiles partials
+      const double parts = std::max(1.0, static_cast<double>(units) / static_cast<double>(tiles));
+      t = (std::ceil(iters / static_cast<double>(units)) * kb_cycles + epi + parts * 3000.0 * (c.cg * c.bn_cta) / 256.0) /
+          eff;
+    }
     if (t < best_t * 0.999) {
       best_t = t;
       best = c;
+      best.streamk = sk;
     }
   }
   return best;

@@ -39,6 +39,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "ptx.cuh"
@@ -51,6 +52,7 @@ constexpr int kBMCta = 128;        // A rows per CTA
 constexpr int kThreads = 512;
 constexpr int kSplitThreads = 128;
 constexpr int kEpiWarps = 8;
+constexpr int kEpiStride = 20;     // floats per staged row (16 data + 4 pad: 16-B aligned, few bank conflicts)
 constexpr int kKcBlocksDefault = 4;   // K_c = 4 * 32 = 128: RZ partial length before RN promotion
 constexpr int kGroupMDefault = 8;     // raster: tile-rows per group (L2 reuse)
 
@@ -78,18 +80,39 @@ struct TcCfg {
   static constexpr int kRawBytes = kRaw * (kABytes + kBBytes);
   static constexpr int kLoBytes = SPLIT3 ? kLo * (kABytes + kBBytes) : 0;
   static constexpr int kNumBars = 2 * kRaw + 2 * kLo + 4;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + kRawBytes + kLoBytes + kNumBars * 8 + 16;
+  static constexpr int kEpiStageBytes = kEpiWarps * 32 * kEpiStride * 4;  // transpose staging
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kRawBytes + kLoBytes + kEpiStageBytes + kNumBars * 8 + 16;
 };
 
 struct TcParams {
+  const float* A;  // raw pointers for L2 prefetch (the TMA maps carry the same tensors)
+  long long lda;
   int m, n, k;
   int tiles_m, tiles_n, num_tiles, kblocks;
   int kc_blocks;  // K-blocks per TMEM partial (K_c / 32)
   int group_m;    // raster group height in tiles
+  // stream-K: the tiles x kblocks iteration space is cut
+  // into equal contiguous ranges, one per cluster; tiles split between clusters
+  // are reduced in a fixed order through a workspace (deterministic).
+  int streamk;
+  long long iters;         // num_tiles * kblocks
+  float* ws;               // [clusters][CG][128][kMmaN] fp32 partials
+  unsigned* flags;         // [clusters][CG][kEpiWarps] epoch flags
+  unsigned epoch;          // this launch's flag value
   float alpha, beta;
   float* C;
   long long ldc;
+  unsigned long long* trace;  // debug timeline [grid][kTraceSlots] (%globaltimer ns) or null
 };
+
+constexpr int kTraceSlots = 8;
+__device__ __forceinline__ void trace_mark(const TcParams& p, int slot) {
+  if (p.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * kTraceSlots + slot] = t;
+  }
+}
 
 // lo part of the 3xTF32 split of one fp32 value x (bit pattern):
 //   hi = x with the low 13 mantissa bits cleared (what kind::tf32 reads from a
@@ -133,39 +156,118 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   tn_ = r / gsize;
 }
 
+// Work units: (tile, K-block range).  Data-parallel: whole tiles c, c+C, ...
+// Stream-K: cluster c owns iterations [c*I/C, (c+1)*I/C) of I = tiles x
+// kblocks; its first unit may start inside a tile (a "partial" unit, written to
+// the workspace), its last may end inside one (the tile's "finalizer", which
+// adds the later clusters' partials in cluster order).
+struct Unit {
+  int tile, kb0, kb1;
+};
+struct UnitIter {
+  long long it, end;  // stream-K cursor
+  int next_tile;      // data-parallel cursor
+};
+__device__ __forceinline__ long long sk_start(long long iters, int c, int C) { return iters * c / C; }
+__device__ __forceinline__ UnitIter units_begin(const TcParams& p, int cluster, int C) {
+  UnitIter u;
+  u.it = p.streamk ? sk_start(p.iters, cluster, C) : 0;
+  u.end = p.streamk ? sk_start(p.iters, cluster + 1, C) : 0;
+  u.next_tile = cluster;
+  return u;
+}
+__device__ __forceinline__ bool units_next(const TcParams& p, int C, UnitIter& s, Unit& u) {
+  if (!p.streamk) {
+    if (s.next_tile >= p.num_tiles) return false;
+    u.tile = s.next_tile;
+    u.kb0 = 0;
+    u.kb1 = p.kblocks;
+    s.next_tile += C;
+    return true;
+  }
+  if (s.it >= s.end) return false;
+  u.tile = static_cast<int>(s.it / p.kblocks);
+  u.kb0 = static_cast<int>(s.it - static_cast<long long>(u.tile) * p.kblocks);
+  const long long left = s.end - s.it;
+  u.kb1 = (left < p.kblocks - u.kb0) ? u.kb0 + static_cast<int>(left) : p.kblocks;
+  s.it += u.kb1 - u.kb0;
+  return true;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // ------------------------------------------------------------------ epilogue
-// Full tile: all KCOLS columns of this thread's row are inside C:
-// unpredicated 16-byte vector accesses (ldc % 4 == 0 and C 16-B aligned are
-// preconditions of this path).  Partial tile: row/column predicates, nothing
-// outside m x n is touched.
+// C[row0 + r, col0 + j] = alpha*acc + beta*C for this warp's 32 rows x KCOLS
+// columns, where lane r holds row r (the TMEM lane mapping).  Coalescing: each
+// 16-column slab is transposed through a per-warp shared-memory stage so that
+// every warp-wide access covers 8 rows x 64 contiguous bytes (8 L1 wavefronts)
+// instead of 32 rows x 16 bytes.  Full/partial tile separation: a 4-column
+// group entirely inside C uses one 16-byte vector access; groups crossing the
+// right edge, and rows past m, are predicated element by element -- nothing
+// outside m x n is read or written.  beta == 0 never reads C.
 template <int KCOLS>
-__device__ __forceinline__ void epi_store(float* __restrict__ crow, const float (&acc)[KCOLS], bool full_row,
-                                          int ncols, float alpha, float beta) {
-  if (full_row) {
-    float4* c4 = reinterpret_cast<float4*>(crow);
-    if (beta == 0.0f) {
+__device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, int m, int n, int row0, int col0,
+                                          const float (&acc)[KCOLS], float alpha, float beta, float* stage,
+                                          int lane) {
 #pragma unroll
-      for (int q = 0; q < KCOLS / 4; ++q)
-        c4[q] = make_float4(alpha * acc[4 * q], alpha * acc[4 * q + 1], alpha * acc[4 * q + 2], alpha * acc[4 * q + 3]);
-    } else {
+  for (int c = 0; c < KCOLS; c += 16) {
 #pragma unroll
-      for (int q0 = 0; q0 < KCOLS / 4; q0 += 4) {
-        float4 c[4];
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(stage + lane * kEpiStride + j) =
+          make_float4(acc[c + j], acc[c + j + 1], acc[c + j + 2], acc[c + j + 3]);
+    __syncwarp();
+    const int cc = (lane & 3) * 4;
+    const int col = col0 + c + cc;
+    const bool full_cols = col + 3 < n;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) c[q] = c4[q0 + q];
+    for (int i0 = 0; i0 < 4; i0 += 2) {  // two 8-row groups per round: 2 C loads in flight, low register use
+      float4 v[2], cv[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int j = 4 * (q0 + q);
-          c4[q0 + q] = make_float4(fmaf(alpha, acc[j], beta * c[q].x), fmaf(alpha, acc[j + 1], beta * c[q].y),
-                                   fmaf(alpha, acc[j + 2], beta * c[q].z), fmaf(alpha, acc[j + 3], beta * c[q].w));
+      for (int i = 0; i < 2; ++i) {
+        const int r = (i0 + i) * 8 + (lane >> 2);
+        v[i] = *reinterpret_cast<const float4*>(stage + r * kEpiStride + cc);
+        cv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int row = row0 + r;
+        if (beta != 0.0f && row < m) {
+          const float* cp = C + static_cast<long long>(row) * ldc + col;
+          if (full_cols) {
+            cv[i] = *reinterpret_cast<const float4*>(cp);
+          } else {
+            if (col < n) cv[i].x = cp[0];
+            if (col + 1 < n) cv[i].y = cp[1];
+            if (col + 2 < n) cv[i].z = cp[2];
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int row = row0 + (i0 + i) * 8 + (lane >> 2);
+        if (row >= m) continue;
+        float4 o;
+        if (beta == 0.0f) {
+          o = make_float4(alpha * v[i].x, alpha * v[i].y, alpha * v[i].z, alpha * v[i].w);
+        } else {
+          o = make_float4(fmaf(alpha, v[i].x, beta * cv[i].x), fmaf(alpha, v[i].y, beta * cv[i].y),
+                          fmaf(alpha, v[i].z, beta * cv[i].z), fmaf(alpha, v[i].w, beta * cv[i].w));
+        }
+        float* cp = C + static_cast<long long>(row) * ldc + col;
+        if (full_cols) {
+          *reinterpret_cast<float4*>(cp) = o;
+        } else {
+          if (col < n) cp[0] = o.x;
+          if (col + 1 < n) cp[1] = o.y;
+          if (col + 2 < n) cp[2] = o.z;
         }
       }
     }
-  } else {
-#pragma unroll
-    for (int j = 0; j < KCOLS; ++j) {
-      if (j < ncols) crow[j] = (beta == 0.0f) ? alpha * acc[j] : fmaf(alpha, acc[j], beta * crow[j]);
-    }
+    __syncwarp();
   }
 }
 
@@ -181,7 +283,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* rawB = rawA + RAW * Cfg::kABytes;
   uint8_t* loA = rawB + RAW * Cfg::kBBytes;
   uint8_t* loB = loA + (SPLIT3 ? LO * Cfg::kABytes : 0);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRawBytes + Cfg::kLoBytes);
+  float* epi_stage = reinterpret_cast<float*>(smem + Cfg::kRawBytes + Cfg::kLoBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRawBytes + Cfg::kLoBytes + Cfg::kEpiStageBytes);
   uint64_t* full = bars;                   // [RAW] TMA landed (local)
   uint64_t* empty_raw = full + RAW;        // [RAW] MMA done with raw stage (commit, multicast)
   uint64_t* ready = empty_raw + RAW;       // [LO]  split done in all CTAs (leader)
@@ -195,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0;
   const int cluster_id = blockIdx.x / CG;
   const int num_clusters = gridDim.x / CG;
+  if (threadIdx.x == 0) trace_mark(p, 0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < RAW; ++i) {
@@ -221,20 +325,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  if (threadIdx.x == 0) trace_mark(p, 1);
 
   if (warp < 4) {
-    ptx::setmaxnreg_dec<80>();
+    ptx::setmaxnreg_dec<72>();
     if (warp == 0) {
       // ---------------------------------------------------------- producer
       if (ptx::elect_one()) {
         int s = 0;
         uint32_t ph = 0;
-        for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+        UnitIter ui = units_begin(p, cluster_id, num_clusters);
+        Unit u;
+        while (units_next(p, num_clusters, ui, u)) {
           int tmi, tni;
-          tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, tmi, tni);
+          tile_coords(u.tile, p.tiles_m, p.tiles_n, p.group_m, tmi, tni);
           const int row0 = tmi * Cfg::kTileM + static_cast<int>(rank) * kBMCta;
           const int col0 = tni * Cfg::kTileN + static_cast<int>(rank) * BN_CTA;
-          for (int kb = 0; kb < p.kblocks; ++kb) {
+          const int rows_here = min(kBMCta, p.m - row0);
+          for (int kb = u.kb0; kb < u.kb1; ++kb) {
+            if (kb == max(u.kb0, u.kb1 - p.kc_blocks) && u.kb1 == p.kblocks && p.beta != 0.0f && rows_here > 0) {
+              // This unit's epilogue will read beta*C: stage this CTA's C rows
+              // in L2 about one K_c chunk (plus the ring depth) ahead, so the
+              // epilogue's loads hit L2 instead of exposing DRAM latency.
+              const int c0 = tni * Cfg::kTileN;
+              const int cols = min(Cfg::kTileN, p.n - c0);
+              const uint32_t bytes = static_cast<uint32_t>(cols * 4) & ~15u;  // floor: never past the row
+              if (bytes)
+                for (int r = 0; r < rows_here; ++r) ptx::prefetch_l2_bulk(p.C + (row0 + r) * p.ldc + c0, bytes);
+            }
             ptx::mbar_wait(&empty_raw[s], ph ^ 1);
             ptx::mbar_arrive_expect_tx(&full[s], Cfg::kABytes + Cfg::kBBytes);
             ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * kBK, row0);
@@ -244,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++s == RAW) { s = 0; ph ^= 1; }
           }
         }
+        trace_mark(p, 2);  // producer done issuing
       }
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
@@ -253,15 +372,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t loA_s = ptx::smem_u32(loA), loB_s = ptx::smem_u32(loB);
         int s = 0, sl = 0, pb = 0;
         uint32_t ph = 0, phl = 0, pph = 0;
-        for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-          for (int kb0 = 0; kb0 < p.kblocks; kb0 += p.kc_blocks) {
-            const int kb1 = min(kb0 + p.kc_blocks, p.kblocks);
+        UnitIter ui = units_begin(p, cluster_id, num_clusters);
+        Unit u;
+        while (units_next(p, num_clusters, ui, u)) {
+          for (int kb0 = u.kb0; kb0 < u.kb1; kb0 += p.kc_blocks) {
+            const int kb1 = min(kb0 + p.kc_blocks, u.kb1);
             ptx::mbar_wait_cluster(&part_empty[pb], pph ^ 1);
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + static_cast<uint32_t>(pb * Cfg::kMmaN);
             for (int kb = kb0; kb < kb1; ++kb) {
               ptx::mbar_wait_cluster(&ready[sl], phl);
               ptx::tc_fence_after();
+              if (kb == 0 && s == 0 && ph == 0) trace_mark(p, 4);  // first MMA issue
 #pragma unroll
               for (int ks = 0; ks < kBK / 8; ++ks) {
                 // A: K-major SW128, K step of 8 tf32 = 32 B inside the swizzle row.
@@ -291,18 +413,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++pb == 2) { pb = 0; pph ^= 1; }
           }
         }
+        trace_mark(p, 5);  // last MMA issued
       }
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ split
-    ptx::setmaxnreg_dec<80>();
+    ptx::setmaxnreg_dec<72>();
     const int st = threadIdx.x - 128;
     const uint32_t rawA_s = ptx::smem_u32(rawA), rawB_s = ptx::smem_u32(rawB);
     const uint32_t loA_s = ptx::smem_u32(loA), loB_s = ptx::smem_u32(loB);
     int s = 0, sl = 0;
     uint32_t ph = 0, phl = 0;
-    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-      for (int kb = 0; kb < p.kblocks; ++kb) {
+    UnitIter ui = units_begin(p, cluster_id, num_clusters);
+    Unit u;
+    while (units_next(p, num_clusters, ui, u)) {
+      for (int kb = u.kb0; kb < u.kb1; ++kb) {
         ptx::mbar_wait(&full[s], ph);
         // The ready ring must not run more than LO stages ahead of the MMA
         // (an mbarrier phase may not complete twice before it is observed).
@@ -323,18 +448,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ promotion + epilogue
-    ptx::setmaxnreg_inc<176>();
+    ptx::setmaxnreg_inc<184>();
     const int q = warp & 3;             // TMEM lane quarter (rows 32q..32q+31 of this CTA)
     const int h = (warp - 8) >> 2;      // column half
     int pb = 0;
     uint32_t pph = 0;
-    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+    UnitIter ui = units_begin(p, cluster_id, num_clusters);
+    Unit u;
+    const int wslot = (static_cast<int>(rank) * kEpiWarps + (warp - 8));  // flag slot within a cluster
+    while (units_next(p, num_clusters, ui, u)) {
       int tmi, tni;
-      tile_coords(t, p.tiles_m, p.tiles_n, p.group_m, tmi, tni);
+      tile_coords(u.tile, p.tiles_m, p.tiles_n, p.group_m, tmi, tni);
       float acc[KCOLS];
 #pragma unroll
       for (int j = 0; j < KCOLS; ++j) acc[j] = 0.0f;
-      for (int kb0 = 0; kb0 < p.kblocks; kb0 += p.kc_blocks) {
+      for (int kb0 = u.kb0; kb0 < u.kb1; kb0 += p.kc_blocks) {
         ptx::mbar_wait(&part_full[pb], pph);
         ptx::tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
@@ -355,13 +483,58 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (++pb == 2) { pb = 0; pph ^= 1; }
       }
-      const int row = tmi * Cfg::kTileM + static_cast<int>(rank) * kBMCta + q * 32 + lane;
-      const int col0 = tni * Cfg::kTileN + h * KCOLS;
-      if (row < p.m && col0 < p.n) {
-        const bool full_row = (col0 + KCOLS <= p.n);
-        epi_store<KCOLS>(p.C + static_cast<long long>(row) * p.ldc + col0, acc, full_row, p.n - col0, p.alpha,
-                         p.beta);
+      // Workspace slice of this warp in a cluster's partial: [rank][warp][KCOLS/4][32 lanes] float4,
+      // so every warp-wide access is 512 contiguous bytes; the same warp/lane of
+      // every cluster uses the same offsets, so partials line up element by element.
+      const long long ws_off = ((static_cast<long long>(rank) * kEpiWarps + (warp - 8)) * (KCOLS / 4)) * 32 + lane;
+      const long long ws_stride = static_cast<long long>(CG) * kEpiWarps * (KCOLS / 4) * 32;  // float4 per cluster
+      if (u.kb0 > 0) {
+        // partial unit: publish the fp32 partial, then the epoch flag
+        float4* w = reinterpret_cast<float4*>(p.ws) + cluster_id * ws_stride + ws_off;
+#pragma unroll
+        for (int j = 0; j < KCOLS / 4; ++j)
+          w[j * 32] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(p.flags + cluster_id * (CG * kEpiWarps) + wslot, p.epoch);
+        continue;
       }
+      if (u.kb1 < p.kblocks) {
+        // finalizer: add the partials of the clusters that own the rest of this
+        // tile, in increasing cluster order (fixed order -> deterministic)
+        const long long tile_end = static_cast<long long>(u.tile + 1) * p.kblocks;
+        for (int c2 = cluster_id + 1; c2 < num_clusters && sk_start(p.iters, c2, num_clusters) < tile_end; ++c2) {
+          const unsigned* f = p.flags + c2 * (CG * kEpiWarps) + wslot;
+          if (lane == 0) {
+            while (ld_acquire_gpu(f) != p.epoch) __nanosleep(64);
+          }
+          __syncwarp();
+          const unsigned seen = ld_acquire_gpu(f);  // every lane acquires (orders its own loads below)
+          (void)seen;
+          const float4* w = reinterpret_cast<const float4*>(p.ws) + c2 * ws_stride + ws_off;
+          constexpr int kGrp = (KCOLS / 4) < 8 ? (KCOLS / 4) : 8;
+#pragma unroll
+          for (int j0 = 0; j0 < KCOLS / 4; j0 += kGrp) {
+            float4 v[kGrp];
+#pragma unroll
+            for (int j = 0; j < kGrp; ++j) v[j] = __ldcg(w + (j0 + j) * 32);
+#pragma unroll
+            for (int j = 0; j < kGrp; ++j) {
+              acc[4 * (j0 + j)] += v[j].x;
+              acc[4 * (j0 + j) + 1] += v[j].y;
+              acc[4 * (j0 + j) + 2] += v[j].z;
+              acc[4 * (j0 + j) + 3] += v[j].w;
+            }
+          }
+        }
+      }
+      const int wrow0 = tmi * Cfg::kTileM + static_cast<int>(rank) * kBMCta + q * 32;
+      const int col0 = tni * Cfg::kTileN + h * KCOLS;
+      if (warp == 8 && lane == 0) trace_mark(p, 6);  // accumulation of this unit done
+      if (wrow0 < p.m && col0 < p.n)
+        epi_store<KCOLS>(p.C, p.ldc, p.m, p.n, wrow0, col0, acc, p.alpha, p.beta,
+                         epi_stage + (warp - 8) * 32 * kEpiStride, lane);
+      if (warp == 8 && lane == 0) trace_mark(p, 7);  // epilogue of this unit done
     }
   }
 
@@ -413,7 +586,7 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, 
 }
 
 template <int CG, int BN_CTA, bool SPLIT3>
-tm_status launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t stream) {
+tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t stream) {
   using Cfg = TcCfg<CG, BN_CTA, SPLIT3>;
   auto kern = k_sgemm_tc<CG, BN_CTA, SPLIT3>;
   static bool attr_set = false;  // per instantiation; attribute is per-function, process-wide
@@ -427,6 +600,8 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t stream) {
   if (!encode_2d(&tmA, a.A, a.m, a.k, a.lda, kBK, kBMCta, CU_TENSOR_MAP_SWIZZLE_128B)) return TM_ERR_INTERNAL;
   if (!encode_2d(&tmB, a.B, a.k, a.n, a.ldb, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return TM_ERR_INTERNAL;
   TcParams p;
+  p.A = a.A;
+  p.lda = a.lda;
   p.m = static_cast<int>(a.m);
   p.n = static_cast<int>(a.n);
   p.k = static_cast<int>(a.k);
@@ -443,7 +618,21 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t stream) {
   p.C = a.C;
   p.ldc = a.ldc;
   const int max_clusters = num_sms / CG;
-  const int clusters = p.num_tiles < max_clusters ? p.num_tiles : max_clusters;
+  int clusters = p.num_tiles < max_clusters ? p.num_tiles : max_clusters;
+  p.iters = static_cast<long long>(p.num_tiles) * p.kblocks;
+  p.streamk = 0;
+  p.ws = nullptr;
+  p.flags = nullptr;
+  p.epoch = 0;
+  if (streamk) {
+    clusters = max_clusters;
+    if (p.iters < 2LL * clusters) clusters = static_cast<int>(p.iters / 2 > 0 ? p.iters / 2 : 1);
+    const size_t ws_bytes = static_cast<size_t>(clusters) * CG * kBMCta * Cfg::kMmaN * 4;
+    const size_t flag_count = static_cast<size_t>(clusters) * CG * kEpiWarps;
+    tm_status st = streamk_workspace(stream, ws_bytes, flag_count, &p.ws, &p.flags, &p.epoch);
+    if (st != TM_OK) return st;
+    p.streamk = 1;
+  }
 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CG, 1, 1);
@@ -457,20 +646,41 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  p.trace = nullptr;
+  const char* trace_path = std::getenv("TM_TRACE_PATH");  // debug timeline (bench/profiling only)
+  if (trace_path) {
+    if (cudaMalloc(&p.trace, sizeof(unsigned long long) * kTraceSlots * clusters * CG) != cudaSuccess) return TM_ERR_CUDA;
+    cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * kTraceSlots * clusters * CG, stream);
+  }
   if (cudaLaunchKernelEx(&cfg, kern, tmA, tmB, p) != cudaSuccess) return TM_ERR_CUDA;
+  if (trace_path) {
+    const int n = kTraceSlots * clusters * CG;
+    unsigned long long* h = new unsigned long long[n];
+    cudaStreamSynchronize(stream);
+    cudaMemcpy(h, p.trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
+    cudaFree(p.trace);
+    if (FILE* f = std::fopen(trace_path, "a")) {
+      std::fprintf(f, "{\"cg\":%d,\"bn\":%d,\"sk\":%d,\"m\":%d,\"n\":%d,\"k\":%d,\"ctas\":%d,\"t\":[", CG, BN_CTA,
+                   p.streamk, p.m, p.n, p.k, clusters * CG);
+      for (int i = 0; i < n; ++i) std::fprintf(f, "%s%llu", i ? "," : "", h[i]);
+      std::fprintf(f, "]}\n");
+      std::fclose(f);
+    }
+    delete[] h;
+  }
   return TM_OK;
 }
 
 template <bool SPLIT3>
-tm_status launch_split(const GemmArgs& a, int cg, int bn, int num_sms, cudaStream_t s) {
+tm_status launch_split(const GemmArgs& a, int cg, int bn, int num_sms, bool sk, cudaStream_t s) {
   if (cg == 2) {
-    if (bn == 128) return launch_cfg<2, 128, SPLIT3>(a, num_sms, s);
-    if (bn == 64) return launch_cfg<2, 64, SPLIT3>(a, num_sms, s);
-    if (bn == 32) return launch_cfg<2, 32, SPLIT3>(a, num_sms, s);
+    if (bn == 128) return launch_cfg<2, 128, SPLIT3>(a, num_sms, sk, s);
+    if (bn == 64) return launch_cfg<2, 64, SPLIT3>(a, num_sms, sk, s);
+    if (bn == 32) return launch_cfg<2, 32, SPLIT3>(a, num_sms, sk, s);
   } else if (cg == 1) {
-    if (bn == 128) return launch_cfg<1, 128, SPLIT3>(a, num_sms, s);
-    if (bn == 64) return launch_cfg<1, 64, SPLIT3>(a, num_sms, s);
-    if (bn == 32) return launch_cfg<1, 32, SPLIT3>(a, num_sms, s);
+    if (bn == 128) return launch_cfg<1, 128, SPLIT3>(a, num_sms, sk, s);
+    if (bn == 64) return launch_cfg<1, 64, SPLIT3>(a, num_sms, sk, s);
+    if (bn == 32) return launch_cfg<1, 32, SPLIT3>(a, num_sms, sk, s);
   }
   return TM_ERR_INVALID_VALUE;
 }
@@ -479,8 +689,8 @@ tm_status launch_split(const GemmArgs& a, int cg, int bn, int num_sms, cudaStrea
 
 tm_status launch_tc(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream) {
   if (a.m > INT32_MAX / 2 || a.n > INT32_MAX / 2 || a.k > INT32_MAX / 2) return TM_ERR_INVALID_VALUE;
-  return c.split3 ? launch_split<true>(a, c.cg, c.bn_cta, num_sms, stream)
-                  : launch_split<false>(a, c.cg, c.bn_cta, num_sms, stream);
+  return c.split3 ? launch_split<true>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream)
+                  : launch_split<false>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
 }
 
 }  // namespace tmk

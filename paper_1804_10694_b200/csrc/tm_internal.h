@@ -25,13 +25,22 @@ struct TcChoice {
   int cg;
   int bn_cta;
   bool split3;
+  bool streamk;  // stream-K decomposition (wave-quantized shapes)
 };
 
 tm_status launch_tc(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream);
 tm_status launch_simt(const GemmArgs& a, cudaStream_t stream);
 tm_status launch_scale(int64_t m, int64_t n, float beta, float* C, int64_t ldc, cudaStream_t stream);
 
+// Library-owned stream-K workspace for `stream` on the current device: at least
+// ws_bytes of fp32 partials and flag_count epoch flags; *epoch is the value this
+// launch must write (flags hold earlier epochs, never the new one).
+tm_status streamk_workspace(cudaStream_t stream, size_t ws_bytes, size_t flag_count, float** ws, unsigned** flags,
+                            unsigned* epoch);
+
 // Picks the tensor-core configuration for a shape (planner, plan.cpp).
 TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms);
+// Whether a configuration should run stream-K for this shape.
+bool plan_streamk(int64_t m, int64_t n, int64_t k, int cg, int bn_cta, int num_sms);
 
 }  // namespace tmk

@@ -184,3 +184,26 @@ def test_large_k_accuracy_sampled_rows(cfg, kind):
     del dA, dB, dC
     R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0, rows=rows)
     assert float(np.max(oracle.normalized_error(C, R, D))) <= TOL
+
+
+@pytest.mark.parametrize("config", ["2,128,1", "2,64,1", "2,32,1", "1,128,1", "1,64,1", "1,32,1"])
+@pytest.mark.parametrize("shape", [(1060, 1060, 1060), (300, 260, 5000), (777, 1000, 3000), (129, 65, 64)])
+def test_streamk_fixed_order_reduction(config, shape):
+    """Stream-K (tiles split across clusters, partials reduced in cluster
+    order through the workspace): parity and run-to-run bit-determinism."""
+    m, n, k = shape
+    pad = lambda x: (x + 3) // 4 * 4
+    lda, ldb, ldc = pad(k), pad(n), pad(n)
+    A, B, C0 = si.matrices(m, n, k, seed=m + n + k, lda=lda, ldb=ldb, ldc=ldc)
+    C1, _ = run(A, B, C0, si.ALPHA, si.BETA, TF32X3, lda=lda, ldb=ldb, ldc=ldc, config=config)
+    C2, _ = run(A, B, C0, si.ALPHA, si.BETA, TF32X3, lda=lda, ldb=ldb, ldc=ldc, config=config)
+    assert np.array_equal(C1, C2)
+    assert max_err(C1, A, B, C0, si.ALPHA, si.BETA) <= TOL
+
+
+def test_streamk_integer_bit_exact():
+    m, n, k = 900, 700, 1500
+    A, B, C0 = si.matrices(m, n, k, 13, kind="integer")
+    C, _ = run(A, B, C0, 1.5, 0.5, TF32X3, config="2,128,1")
+    R, _ = oracle.sgemm(1.5, A, B, 0.5, C0)
+    assert np.array_equal(C.astype(np.float64), R)
