@@ -44,6 +44,23 @@ def load_peaks():
             "source": "fallback (B200_PROFILING.md)"}
 
 
+def ncu_traffic(config, path, world):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed `ncu --set full` capture of this workload (profiles/ncu_traffic_*.json),
+    or None when no capture matches (e.g. per-rank shards at N > 1)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_traffic_r*.json")))
+    if not files or world != 1:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    key = config if path != "simt" else f"{config}:simt"
+    if key not in d:
+        return None, None
+    e = d[key]
+    return e["dram_read_bytes"] + e["dram_write_bytes"], os.path.relpath(files[-1], ROOT)
+
+
 def roofline_peak(path, peaks):
     """(bound, peak, unit, note).  3xTF32: measured bf16 dense peak x nominal
     tf32/bf16 ratio (1.1/2.25) / 3 MMAs per fp32 product.  SIMT: FFMA peak from
@@ -298,8 +315,10 @@ def main():
         peak_note = peaks["source"] + " hbm_gbs"
     else:
         achieved = my_flops / (my_ms * 1e-3) / 1e12
+    traffic, traffic_src = ncu_traffic(args.config, path, world)
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
-            "frac": round(achieved / peak, 4), "traffic": None, "kernel": f"k_sgemm_tc ({path})" if kernel != "simt"
+            "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_unit": "bytes per launch",
+            "traffic_source": traffic_src, "kernel": f"k_sgemm_tc ({path})" if kernel != "simt"
             else "k_sgemm_simt", "peak_source": peak_note}
     if bound == "tensor":
         sus = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / 3.0

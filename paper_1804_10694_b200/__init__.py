@@ -97,11 +97,20 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+_raw_stream = None
+
+
 def _stream(stream):
+    """cudaStream_t of `stream` (int / torch.cuda.Stream) or torch's current stream."""
+    global _raw_stream
     if stream is not None:
-        return ctypes.c_void_p(int(stream))
+        return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
     import torch
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if _raw_stream is None:
+        get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        _raw_stream = (lambda: get(torch.cuda.current_device())) if get else \
+            (lambda: torch.cuda.current_stream().cuda_stream)
+    return ctypes.c_void_p(_raw_stream())
 
 
 def _f32(name, t):

@@ -54,7 +54,7 @@ constexpr int kSplitThreads = 128;
 constexpr int kEpiWarps = 8;
 constexpr int kEpiStride = 20;     // floats per staged row (16 data + 4 pad: 16-B aligned, few bank conflicts)
 constexpr int kKcBlocksDefault = 4;   // K_c = 4 * 32 = 128: RZ partial length before RN promotion
-constexpr int kGroupMDefault = 8;     // raster: tile-rows per group (L2 reuse)
+constexpr int kGroupMDefault = 16;    // raster: tile-rows per group (L2 reuse)
 
 template <int BN_CTA>
 struct StageCfg;
@@ -609,10 +609,11 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t 
   p.tiles_n = static_cast<int>((a.n + Cfg::kTileN - 1) / Cfg::kTileN);
   p.num_tiles = p.tiles_m * p.tiles_n;
   p.kblocks = static_cast<int>((a.k + kBK - 1) / kBK);
-  p.kc_blocks = kKcBlocksDefault;
-  p.group_m = kGroupMDefault;
-  if (const char* e = std::getenv("TM_KC_BLOCKS")) p.kc_blocks = std::max(1, std::atoi(e));  // tuning knob
-  if (const char* e = std::getenv("TM_GROUP_M")) p.group_m = std::max(1, std::atoi(e));     // tuning knob
+  // Tuning knobs (bench/tests only), read once per process.
+  static const int env_kc = [] { const char* e = std::getenv("TM_KC_BLOCKS"); return e ? std::max(1, std::atoi(e)) : 0; }();
+  static const int env_gm = [] { const char* e = std::getenv("TM_GROUP_M"); return e ? std::max(1, std::atoi(e)) : 0; }();
+  p.kc_blocks = env_kc ? env_kc : kKcBlocksDefault;
+  p.group_m = env_gm ? env_gm : kGroupMDefault;
   p.alpha = a.alpha;
   p.beta = a.beta;
   p.C = a.C;
