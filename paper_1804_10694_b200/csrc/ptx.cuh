@@ -186,25 +186,28 @@ __device__ __forceinline__ void tc_fence_after() {
 }
 
 // D[tmem] (+)= A[smem] * B[smem], kind::tf32, fp32 accumulate.
-template <int CG>
+// COLL: A-operand collector usage -- 0 discard (default), 1 fill (read A and
+// keep it in the collector), 2 lastuse (reuse the kept A, then release), so
+// two consecutive MMAs with the same A read it from shared memory once.
+#define TM_MMA_TF32(CGS, COLLS)                                                                         \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                                    \
+               "tcgen05.mma.cta_group::" CGS ".kind::tf32" COLLS " [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem), \
+               "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)                                    \
+               : "memory")
+template <int CG, int COLL = 0>
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                          uint32_t accumulate) {
   if constexpr (CG == 1) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
+    if constexpr (COLL == 1) TM_MMA_TF32("1", ".collector::a::fill");
+    else if constexpr (COLL == 2) TM_MMA_TF32("1", ".collector::a::lastuse");
+    else TM_MMA_TF32("1", "");
   } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
+    if constexpr (COLL == 1) TM_MMA_TF32("2", ".collector::a::fill");
+    else if constexpr (COLL == 2) TM_MMA_TF32("2", ".collector::a::lastuse");
+    else TM_MMA_TF32("2", "");
   }
 }
+#undef TM_MMA_TF32
 
 // Arrive on `bar` once all previously issued MMAs of this thread complete.
 // CG == 2: multicast the arrive to the same barrier in every CTA of `mask`.

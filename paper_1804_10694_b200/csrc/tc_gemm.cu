@@ -61,9 +61,9 @@ struct StageCfg;
 template <>
 struct StageCfg<128> { static constexpr int kRaw = 4, kLo = 2; };
 template <>
-struct StageCfg<64> { static constexpr int kRaw = 5, kLo = 3; };
+struct StageCfg<64> { static constexpr int kRaw = 6, kLo = 2; };
 template <>
-struct StageCfg<32> { static constexpr int kRaw = 6, kLo = 3; };
+struct StageCfg<32> { static constexpr int kRaw = 8, kLo = 2; };
 
 template <int CG, int BN_CTA, bool SPLIT3>
 struct TcCfg {
@@ -397,9 +397,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const uint64_t aL = ptx::sdesc(loA_s + sl * Cfg::kABytes + ks * 32, 16, 1024, ptx::kLayoutSW128);
                   const uint64_t bL =
                       ptx::sdesc(loB_s + sl * Cfg::kBBytes + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
+                  // A_hi feeds two MMAs back to back: fetched from smem once (collector fill/lastuse)
                   ptx::mma_tf32<CG>(d, aL, bH, idesc, acc);
-                  ptx::mma_tf32<CG>(d, aH, bL, idesc, 1u);
-                  ptx::mma_tf32<CG>(d, aH, bH, idesc, 1u);
+                  ptx::mma_tf32<CG, 1>(d, aH, bL, idesc, 1u);
+                  ptx::mma_tf32<CG, 2>(d, aH, bH, idesc, 1u);
                 } else {
                   ptx::mma_tf32<CG>(d, aH, bH, idesc, acc);
                 }
