@@ -128,7 +128,7 @@ Plan make_plan(const GemmArgs& a, int algo, int num_sms) {
   return pl;
 }
 
-tm_status run(const GemmArgs& a, int algo, cudaStream_t stream) {
+tm_status run(const GemmArgs& a, int algo, cudaStream_t stream, int sm_reserve = 0) {
   // Host-side validation first: invalid arguments never touch the device.
   Plan pre = make_plan(a, algo, 148);
   if (pre.path == Path::kInvalid) return TM_ERR_INVALID_VALUE;
@@ -136,7 +136,10 @@ tm_status run(const GemmArgs& a, int algo, cudaStream_t stream) {
   DevInfo* dev = nullptr;
   tm_status st = current_device(&dev);
   if (st != TM_OK) return st;
-  Plan pl = make_plan(a, algo, dev->sms);
+  // sm_reserve: SMs left free for concurrent kernels (the distributed mode's
+  // NCCL broadcast must be able to run beside the persistent GEMM).
+  const int sms = (sm_reserve > 0 && dev->sms - sm_reserve >= 2) ? dev->sms - sm_reserve : dev->sms;
+  Plan pl = make_plan(a, algo, sms);
   if (log_enabled())
     std::fprintf(stderr, "[tm] sgemm m=%lld n=%lld k=%lld algo=%d -> %s cg=%d bn=%d split3=%d\n",
                  static_cast<long long>(a.m), static_cast<long long>(a.n), static_cast<long long>(a.k), algo,
@@ -149,7 +152,7 @@ tm_status run(const GemmArgs& a, int algo, cudaStream_t stream) {
     case Path::kSimt:
       return launch_simt(a, stream);
     case Path::kTc:
-      return launch_tc(a, pl.tc, dev->sms, stream);
+      return launch_tc(a, pl.tc, sms, stream);
     default:
       return TM_ERR_INTERNAL;
   }
@@ -204,6 +207,14 @@ std::mutex g_sk_mu;
 std::map<std::pair<int, cudaStream_t>, SkWorkspace> g_sk;
 
 }  // namespace
+
+tm_status sgemm_reserve(const GemmArgs& a, cudaStream_t stream, int sm_reserve) {
+  try {
+    return run(a, TM_ALGO_AUTO, stream, sm_reserve);
+  } catch (...) {
+    return TM_ERR_INTERNAL;
+  }
+}
 
 tm_status streamk_workspace(cudaStream_t stream, size_t ws_bytes, size_t flag_count, float** ws, unsigned** flags,
                             unsigned* epoch) {

@@ -11,9 +11,15 @@
 //
 // NCCL is loaded with dlopen (the same libnccl.so.2 torch uses), so the
 // single-GPU library has no link-time NCCL dependency.
+//
+// SM sharing: the GEMM is a persistent kernel that would occupy every SM (and
+// all registers) for the whole chunk, so a concurrently enqueued NCCL kernel
+// could not start until it finished -- no overlap.  The communicator is created
+// with maxCTAs = kCommCtas and the chunk GEMMs leave kCommCtas SMs free.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -29,10 +35,34 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef enum { ncclSuccess = 0 } ncclResult_t;
 typedef enum { ncclFloat32 = 7 } ncclDataType_t;
+// ncclConfig_t as of NCCL 2.28 (nccl.h ncclConfig_v22800); the size/version
+// fields let older/newer libraries interpret it.
+struct NcclConfig {
+  size_t size;
+  unsigned int magic;
+  unsigned int version;
+  int blocking, cgaClusterSize, minCTAs, maxCTAs;
+  const char* netName;
+  int splitShare, trafficClass;
+  const char* commName;
+  int collnetEnable, CTAPolicy, shrinkShare, nvlsCTAs, nChannelsPerNetPeer, nvlinkCentricSched;
+};
+constexpr int kNcclUndefInt = static_cast<int>(0x80000000);
+constexpr int kCommCtasDefault = 16;
+
+int comm_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("TM_DIST_COMM_SMS");  // tuning knob (bench only)
+    return e ? std::max(0, std::atoi(e)) : kCommCtasDefault;
+  }();
+  return v;
+}
 
 struct Nccl {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, NcclConfig*) = nullptr;
+  ncclResult_t (*GetVersion)(int*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
@@ -52,6 +82,9 @@ void load_nccl() {
   if (!h) return;
   g_nccl.GetUniqueId = reinterpret_cast<decltype(g_nccl.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
   g_nccl.CommInitRank = reinterpret_cast<decltype(g_nccl.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+  g_nccl.CommInitRankConfig =
+      reinterpret_cast<decltype(g_nccl.CommInitRankConfig)>(dlsym(h, "ncclCommInitRankConfig"));
+  g_nccl.GetVersion = reinterpret_cast<decltype(g_nccl.GetVersion)>(dlsym(h, "ncclGetVersion"));
   g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
   g_nccl.Broadcast = reinterpret_cast<decltype(g_nccl.Broadcast)>(dlsym(h, "ncclBroadcast"));
   g_nccl.AllGather = reinterpret_cast<decltype(g_nccl.AllGather)>(dlsym(h, "ncclAllGather"));
@@ -106,7 +139,21 @@ tm_status tm_comm_init(tm_comm_t* out, int nranks, int rank, const tm_unique_id*
   if (cudaGetDevice(&c->device) != cudaSuccess) { delete c; return TM_ERR_CUDA; }
   ncclUniqueId nid;
   std::memcpy(nid.internal, id->bytes, sizeof(nid));
-  if (g_nccl.CommInitRank(&c->comm, nranks, nid, rank) != ncclSuccess) { delete c; return TM_ERR_NCCL; }
+  int ver = 0;
+  if (g_nccl.GetVersion) g_nccl.GetVersion(&ver);
+  ncclResult_t r;
+  if (g_nccl.CommInitRankConfig && ver >= 22800 && comm_ctas() > 0) {
+    NcclConfig cfg = {sizeof(NcclConfig), 0xcafebeef, static_cast<unsigned>(ver),
+                      kNcclUndefInt, kNcclUndefInt, kNcclUndefInt, kNcclUndefInt, nullptr, kNcclUndefInt,
+                      kNcclUndefInt, nullptr, kNcclUndefInt, kNcclUndefInt, kNcclUndefInt, kNcclUndefInt,
+                      kNcclUndefInt, kNcclUndefInt};
+    cfg.maxCTAs = comm_ctas();
+    cfg.minCTAs = std::min(comm_ctas(), 4);
+    r = g_nccl.CommInitRankConfig(&c->comm, nranks, nid, rank, &cfg);
+  } else {
+    r = g_nccl.CommInitRank(&c->comm, nranks, nid, rank);
+  }
+  if (r != ncclSuccess) { delete c; return TM_ERR_NCCL; }
   bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) == cudaSuccess;
   for (int i = 0; ok && i < kMaxChunks; ++i)
@@ -212,8 +259,8 @@ tm_status dist_schedule(int nranks, int rank, int root, int64_t m, int64_t n, in
     const int64_t kr = (k0 + kc <= k) ? kc : k - k0;
     if (cudaStreamWaitEvent(stream, ev_chunk[used], 0) != cudaSuccess) return TM_ERR_CUDA;
     if (rows > 0) {
-      tm_status st = tm_sgemm(rows, n, kr, alpha, A_local + k0, lda, B + k0 * ldb, ldb, k0 == 0 ? beta : 1.0f,
-                              C_local, ldc, stream);
+      tmk::GemmArgs ga{rows, n, kr, alpha, k0 == 0 ? beta : 1.0f, A_local + k0, lda, B + k0 * ldb, ldb, C_local, ldc};
+      tm_status st = tmk::sgemm_reserve(ga, stream, comm_ctas());
       if (st != TM_OK) return st;
     }
   }

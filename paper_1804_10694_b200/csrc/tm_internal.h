@@ -32,6 +32,10 @@ tm_status launch_tc(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStrea
 tm_status launch_simt(const GemmArgs& a, cudaStream_t stream);
 tm_status launch_scale(int64_t m, int64_t n, float beta, float* C, int64_t ldc, cudaStream_t stream);
 
+// tm_sgemm with `sm_reserve` SMs left free (distributed mode, so the NCCL
+// broadcast kernels can run concurrently with the persistent GEMM).
+tm_status sgemm_reserve(const GemmArgs& a, cudaStream_t stream, int sm_reserve);
+
 // Library-owned stream-K workspace for `stream` on the current device: at least
 // ws_bytes of fp32 partials and flag_count epoch flags; *epoch is the value this
 // launch must write (flags hold earlier epochs, never the new one).
