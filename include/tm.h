@@ -158,16 +158,20 @@ tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float a
                         const float* A_local, int64_t lda, float* B, int64_t ldb, int root,
                         float beta, float* C_local, int64_t ldc, void* stream);
 
-/* Single-process loopback of tm_sgemm_dist (verification mode, DESIGN.md
+/* Single-process loopback of the distributed mode (verification, DESIGN.md
  * section 10): emulates `nranks` ranks one after another on the CURRENT device
- * with the identical partition, K-chunk schedule and beta chain; each chunk
- * "broadcast" is a device-to-device copy from Bs[root] into Bs[r].
+ * with the identical partition, schedule and beta chain as the NCCL entry
+ * points; every transfer is a device-to-device copy.
+ *   mode 0: tm_sgemm_dist -- Bs[root] holds B, the other Bs[r] are overwritten
+ *           chunk by chunk ("broadcast").
+ *   mode 1: tm_sgemm_dist_allgather -- Bs[r] holds rank r's k-row shard at rows
+ *           [r*k/P, (r+1)*k/P) (k % nranks == 0); every Bs[r] ends complete.
  *   A_locals[r], Bs[r], C_locals[r]: device pointers (host arrays of nranks),
- *   shaped as tm_sgemm_dist's A_local, B, C_local for rank r.
+ *   shaped as the NCCL entry's A_local, B / B_full, C_local for rank r.
  *   bytes_received: optional host array of nranks counters (bytes each rank's
  *   B received), or NULL.
  * Synchronises `stream`; errors as tm_sgemm_dist. */
-tm_status tm_sgemm_dist_loopback(int nranks, int root, int64_t m, int64_t n, int64_t k, float alpha,
+tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int64_t n, int64_t k, float alpha,
                                  const float* const* A_locals, int64_t lda, float* const* Bs, int64_t ldb,
                                  float beta, float* const* C_locals, int64_t ldc, uint64_t* bytes_received,
                                  void* stream);

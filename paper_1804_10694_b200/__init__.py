@@ -60,7 +60,7 @@ def _load():
     L.tm_comm_rank.argtypes = [vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
     L.tm_comm_bytes_received.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
     L.tm_sgemm_dist.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, i64, ci, f32, vp, i64, vp]
-    L.tm_sgemm_dist_loopback.argtypes = [ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, vp]
+    L.tm_sgemm_dist_loopback.argtypes = [ci, ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, vp]
     L.tm_sgemm_dist_allgather.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, vp, i64, f32, vp, i64, vp]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(L, name)
@@ -200,16 +200,18 @@ def dist_chunks(k: int, nranks: int):
     return out
 
 
-def sgemm_dist_loopback(m, n, k, A_locals, Bs, C_locals, alpha=1.0, beta=0.0, root=0, stream=None):
+def sgemm_dist_loopback(m, n, k, A_locals, Bs, C_locals, alpha=1.0, beta=0.0, root=0, stream=None, allgather=False):
     """Single-process emulation of the row-sharded mode:
     len(A_locals) simulated ranks on the current GPU, same schedule as
-    Comm.sgemm.  Returns the bytes each simulated rank received."""
+    Comm.sgemm (or Comm.sgemm_allgather when allgather=True: Bs[r] holds rank
+    r's k-row shard in place).  Returns the bytes each simulated rank received."""
     P = len(A_locals)
     arr = lambda ts: (ctypes.c_void_p * P)(*[t.data_ptr() for t in ts])
     lda = next((_ld(a) for a in A_locals if a.shape[0] > 0), max(k, 1))
     ldc = next((_ld(c) for c in C_locals if c.shape[0] > 0), max(n, 1))
     got = (ctypes.c_uint64 * P)()
-    st = lib.tm_sgemm_dist_loopback(P, int(root), m, n, k, float(alpha), arr(A_locals), lda, arr(Bs), _ld(Bs[0]),
+    st = lib.tm_sgemm_dist_loopback(P, int(root), 1 if allgather else 0, m, n, k, float(alpha), arr(A_locals), lda,
+                                    arr(Bs), _ld(Bs[0]),
                                     float(beta), arr(C_locals), ldc, got, _stream(stream))
     _check(st, "tm_sgemm_dist_loopback")
     return [int(x) for x in got]

@@ -267,6 +267,48 @@ tm_status dist_schedule(int nranks, int rank, int root, int64_t m, int64_t n, in
   return TM_OK;
 }
 
+// All-gather variant: B arrives pre-sharded by k-rows (rank r owns rows
+// [r*kr, (r+1)*kr), kr = k/P).  The GEMM on the own shard needs no
+// communication and runs first, overlapping the gather (`gather()` enqueues it
+// on comm_stream); the other K ranges follow once it lands.
+template <class Gather>
+tm_status allgather_schedule(int nranks, int rank, int64_t m, int64_t n, int64_t k, float alpha, const float* A_local,
+                             int64_t lda, const float* B_shard, float* B_full, int64_t ldb, float beta,
+                             float* C_local, int64_t ldc, cudaStream_t stream, cudaStream_t comm_stream,
+                             cudaEvent_t ev_start, cudaEvent_t ev_done, uint64_t* bytes_received, Gather&& gather) {
+  if (k % nranks != 0) return TM_ERR_INVALID_VALUE;
+  int64_t row0 = 0, rows = 0;
+  tm_dist_rows(m, nranks, rank, &row0, &rows);
+  const bool reads_ab = alpha != 0.0f && k > 0 && n > 0;
+  if (!reads_ab) return tm_sgemm(rows, n, k, alpha, A_local, lda, B_full, ldb, beta, C_local, ldc, stream);
+  if (!B_shard || !B_full || ldb < (n > 1 ? n : 1)) return TM_ERR_INVALID_VALUE;
+  const int64_t kr = k / nranks, k0 = rank * kr;
+  const int reserve = nranks > 1 ? comm_ctas() : 0;
+  if (cudaEventRecord(ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (cudaStreamWaitEvent(comm_stream, ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
+  const size_t count = static_cast<size_t>(kr) * static_cast<size_t>(ldb);
+  tm_status st = gather(count);
+  if (st != TM_OK) return st;
+  if (bytes_received) *bytes_received += count * 4 * static_cast<uint64_t>(nranks - 1);
+  if (cudaEventRecord(ev_done, comm_stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (rows == 0) return cudaStreamWaitEvent(stream, ev_done, 0) == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+  tmk::GemmArgs own{rows, n, kr, alpha, beta, A_local + k0, lda, B_shard, ldb, C_local, ldc};
+  st = tmk::sgemm_reserve(own, stream, reserve);
+  if (st != TM_OK) return st;
+  if (cudaStreamWaitEvent(stream, ev_done, 0) != cudaSuccess) return TM_ERR_CUDA;
+  if (k0 > 0) {
+    tmk::GemmArgs lo{rows, n, k0, alpha, 1.0f, A_local, lda, B_full, ldb, C_local, ldc};
+    st = tmk::sgemm_reserve(lo, stream, reserve);
+    if (st != TM_OK) return st;
+  }
+  if (k0 + kr < k) {
+    tmk::GemmArgs hi{rows, n, k - k0 - kr, alpha, 1.0f, A_local + k0 + kr, lda, B_full + (k0 + kr) * ldb, ldb, C_local, ldc};
+    st = tmk::sgemm_reserve(hi, stream, reserve);
+    if (st != TM_OK) return st;
+  }
+  return TM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -284,11 +326,12 @@ tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float a
                        &comm->bytes_received, xfer);
 }
 
-tm_status tm_sgemm_dist_loopback(int nranks, int root, int64_t m, int64_t n, int64_t k, float alpha,
+tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int64_t n, int64_t k, float alpha,
                                  const float* const* A_locals, int64_t lda, float* const* Bs, int64_t ldb,
                                  float beta, float* const* C_locals, int64_t ldc, uint64_t* bytes_received,
                                  void* stream_) {
-  if (nranks < 1 || root < 0 || root >= nranks || !A_locals || !Bs || !C_locals || m < 0 || n < 0 || k < 0)
+  if (nranks < 1 || root < 0 || root >= nranks || !A_locals || !Bs || !C_locals || m < 0 || n < 0 || k < 0 ||
+      (mode != 0 && mode != 1))
     return TM_ERR_INVALID_VALUE;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   cudaStream_t cs = nullptr;
@@ -303,17 +346,46 @@ tm_status tm_sgemm_dist_loopback(int nranks, int root, int64_t m, int64_t n, int
     for (int r = 0; r < nranks; ++r) bytes_received[r] = 0;
   // Ranks run one after another on this device; rank r's "broadcast" copies
   // the root's chunk into rank r's B (the root's own transfer is a no-op).
-  for (int r = 0; st == TM_OK && r < nranks; ++r) {
-    const float* root_B = Bs[root];
-    auto xfer = [&](float* p, size_t count) -> tm_status {
-      if (r == root) return TM_OK;
-      const float* src = root_B + (p - Bs[r]);
-      return cudaMemcpyAsync(p, src, count * 4, cudaMemcpyDeviceToDevice, cs) == cudaSuccess ? TM_OK : TM_ERR_CUDA;
-    };
-    st = dist_schedule(nranks, r, root, m, n, k, alpha, A_locals[r], lda, Bs[r], ldb, beta, C_locals[r], ldc, stream,
-                       cs, ev_start, ev_chunk, bytes_received ? &bytes_received[r] : nullptr, xfer);
+  if (mode == 1 && k % nranks != 0) st = TM_ERR_INVALID_VALUE;
+  // All-gather emulation needs every rank's shard before any rank's gather
+  // overwrites the rest of its buffer: keep a copy of all shards.
+  float* shards = nullptr;
+  const int64_t kr = (mode == 1 && nranks > 0) ? k / nranks : 0;
+  if (st == TM_OK && mode == 1 && kr > 0) {
+    if (cudaMalloc(&shards, static_cast<size_t>(k) * ldb * 4) != cudaSuccess) st = TM_ERR_OUT_OF_MEMORY;
+    for (int q = 0; st == TM_OK && q < nranks; ++q)
+      if (cudaMemcpyAsync(shards + q * kr * ldb, Bs[q] + q * kr * ldb, static_cast<size_t>(kr) * ldb * 4,
+                          cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
+        st = TM_ERR_CUDA;
     if (st == TM_OK && cudaStreamSynchronize(stream) != cudaSuccess) st = TM_ERR_CUDA;
   }
+  for (int r = 0; st == TM_OK && r < nranks; ++r) {
+    if (mode == 0) {
+      const float* root_B = Bs[root];
+      auto xfer = [&](float* p, size_t count) -> tm_status {
+        if (r == root) return TM_OK;
+        const float* src = root_B + (p - Bs[r]);
+        return cudaMemcpyAsync(p, src, count * 4, cudaMemcpyDeviceToDevice, cs) == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+      };
+      st = dist_schedule(nranks, r, root, m, n, k, alpha, A_locals[r], lda, Bs[r], ldb, beta, C_locals[r], ldc,
+                         stream, cs, ev_start, ev_chunk, bytes_received ? &bytes_received[r] : nullptr, xfer);
+    } else {
+      auto gather = [&](size_t count) -> tm_status {
+        for (int q = 0; q < nranks; ++q) {
+          if (q == r) continue;
+          if (cudaMemcpyAsync(Bs[r] + q * kr * ldb, shards + q * kr * ldb, count * 4, cudaMemcpyDeviceToDevice, cs) !=
+              cudaSuccess)
+            return TM_ERR_CUDA;
+        }
+        return TM_OK;
+      };
+      st = allgather_schedule(nranks, r, m, n, k, alpha, A_locals[r], lda, Bs[r] + r * kr * ldb, Bs[r], ldb, beta,
+                              C_locals[r], ldc, stream, cs, ev_start, ev_chunk[0],
+                              bytes_received ? &bytes_received[r] : nullptr, gather);
+    }
+    if (st == TM_OK && cudaStreamSynchronize(stream) != cudaSuccess) st = TM_ERR_CUDA;
+  }
+  if (shards) cudaFree(shards);
   if (cs) cudaStreamSynchronize(cs);
   for (int i = 0; i < kMaxChunks; ++i)
     if (ev_chunk[i]) cudaEventDestroy(ev_chunk[i]);
@@ -326,36 +398,14 @@ tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t 
                                   const float* A_local, int64_t lda, const float* B_shard, float* B_full,
                                   int64_t ldb, float beta, float* C_local, int64_t ldc, void* stream_) {
   if (!comm || m < 0 || n < 0 || k < 0) return TM_ERR_INVALID_VALUE;
-  if (k % comm->nranks != 0) return TM_ERR_INVALID_VALUE;
-  int64_t row0 = 0, rows = 0;
-  tm_dist_rows(m, comm->nranks, comm->rank, &row0, &rows);
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  const bool reads_ab = alpha != 0.0f && k > 0 && n > 0;
-  if (!reads_ab) return tm_sgemm(rows, n, k, alpha, A_local, lda, B_full, ldb, beta, C_local, ldc, stream);
-  if (!B_shard || !B_full || ldb < (n > 1 ? n : 1)) return TM_ERR_INVALID_VALUE;
-  const int64_t kr = k / comm->nranks, k0 = comm->rank * kr;
-  if (cudaEventRecord(comm->ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
-  if (cudaStreamWaitEvent(comm->stream, comm->ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
-  const size_t count = static_cast<size_t>(kr) * static_cast<size_t>(ldb);
-  if (g_nccl.AllGather(B_shard, B_full, count, ncclFloat32, comm->comm, comm->stream) != ncclSuccess)
-    return TM_ERR_NCCL;
-  comm->bytes_received += count * 4 * static_cast<uint64_t>(comm->nranks - 1);
-  if (cudaEventRecord(comm->ev_chunk[0], comm->stream) != cudaSuccess) return TM_ERR_CUDA;
-  if (rows == 0) return cudaStreamWaitEvent(stream, comm->ev_chunk[0], 0) == cudaSuccess ? TM_OK : TM_ERR_CUDA;
-  // Own shard first: it is already resident, so it overlaps the all-gather.
-  tm_status st = tm_sgemm(rows, n, kr, alpha, A_local + k0, lda, B_shard, ldb, beta, C_local, ldc, stream);
-  if (st != TM_OK) return st;
-  if (cudaStreamWaitEvent(stream, comm->ev_chunk[0], 0) != cudaSuccess) return TM_ERR_CUDA;
-  if (k0 > 0) {
-    st = tm_sgemm(rows, n, k0, alpha, A_local, lda, B_full, ldb, 1.0f, C_local, ldc, stream);
-    if (st != TM_OK) return st;
-  }
-  if (k0 + kr < k) {
-    st = tm_sgemm(rows, n, k - k0 - kr, alpha, A_local + k0 + kr, lda, B_full + (k0 + kr) * ldb, ldb, 1.0f,
-                  C_local, ldc, stream);
-    if (st != TM_OK) return st;
-  }
-  return TM_OK;
+  auto gather = [&](size_t count) -> tm_status {
+    return g_nccl.AllGather(B_shard, B_full, count, ncclFloat32, comm->comm, comm->stream) == ncclSuccess
+               ? TM_OK
+               : TM_ERR_NCCL;
+  };
+  return allgather_schedule(comm->nranks, comm->rank, m, n, k, alpha, A_local, lda, B_shard, B_full, ldb, beta,
+                            C_local, ldc, static_cast<cudaStream_t>(stream_), comm->stream, comm->ev_start,
+                            comm->ev_chunk[0], &comm->bytes_received, gather);
 }
 
 }  // extern "C"

@@ -5,7 +5,7 @@ as tm_sgemm_dist, with each chunk broadcast replaced by a device copy.
 Checks (SURVEY.md section 4 "Distribution semantics"): each rank's shard equals
 the oracle's rows (PAPER.md:897, rows distributed; no gather, PAPER.md:555-556);
 uneven m % P; P = 1 is bit-identical to tm_sgemm; root != 0; each non-root rank
-receives exactly k*ldb*4 bytes (message conservation)."""
+receives exactly k*ldb*4 bytes (message conservation); the all-gather variant."""
 import numpy as np
 import pytest
 
@@ -98,3 +98,32 @@ def test_loopback_c5_p8_sampled_rows():
     rows = si.sample_rows(m, count=24, tile=2048, extra=bounds)
     R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0, rows=rows)
     assert float(np.max(oracle.normalized_error(C[rows], R, D))) <= TOL
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_loopback_allgather_shards_match_oracle(P):
+    """All-gather variant: B pre-sharded by k-rows (k % P == 0); each rank's
+    GEMM on its own shard overlaps the gather; every rank ends with full B."""
+    import torch
+    import paper_1804_10694_b200 as tm
+    m, n, k = 1060, 260, 1024
+    A, B, C0 = si.matrices(m, n, k, seed=60 + P)
+    dA = torch.from_numpy(np.ascontiguousarray(A)).cuda()
+    kr = k // P
+    Bs, As, Cs, parts = [], [], [], []
+    for r in range(P):
+        r0, rows = tm.dist_rows(m, P, r)
+        parts.append((r0, rows))
+        As.append(dA[r0:r0 + rows])
+        Cs.append(torch.from_numpy(np.ascontiguousarray(C0[r0:r0 + rows])).cuda())
+        buf = torch.full((k, n), float("nan"), dtype=torch.float32, device="cuda")
+        buf[r * kr:(r + 1) * kr] = torch.from_numpy(B[r * kr:(r + 1) * kr]).cuda()
+        Bs.append(buf)
+    got = tm.sgemm_dist_loopback(m, n, k, As, Bs, Cs, si.ALPHA, si.BETA, allgather=True)
+    torch.cuda.synchronize()
+    R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0)
+    for r, ((r0, rows), C) in enumerate(zip(parts, Cs)):
+        e = float(np.max(oracle.normalized_error(C.cpu().numpy(), R[r0:r0 + rows], D[r0:r0 + rows])))
+        assert e <= TOL, (r, e)
+        assert np.array_equal(Bs[r].cpu().numpy(), B)
+        assert got[r] == (P - 1) * kr * n * 4

@@ -207,3 +207,51 @@ def test_streamk_integer_bit_exact():
     C, _ = run(A, B, C0, 1.5, 0.5, TF32X3, config="2,128,1")
     R, _ = oracle.sgemm(1.5, A, B, 0.5, C0)
     assert np.array_equal(C.astype(np.float64), R)
+
+
+@pytest.mark.parametrize("shape", [(1000, 300, 700), (2500, 129, 65), (7, 5, 3)])
+@pytest.mark.parametrize("beta", [0.5, 0.0])
+def test_sgemm_host_end_to_end(shape, beta):
+    """tm_sgemm_host (the e2e leg of bench.py): host buffers with padded
+    leading dimensions, row-block copy/compute overlap, result copied back."""
+    import torch
+    import paper_1804_10694_b200 as tm
+    m, n, k = shape
+    A, B, C0 = si.matrices(m, n, k, seed=sum(shape), lda=k + 3, ldb=n + 1, ldc=n + 2)
+    C = np.array(C0.base if C0.base is not None else C0, copy=True)
+    Cv = C[:, :n]
+    tm.sgemm_host(A, B, Cv, si.ALPHA, beta)
+    assert max_err(Cv, A, B, C0, si.ALPHA, beta) <= TOL
+    assert np.array_equal(C[:, n:], (C0.base if C0.base is not None else C0)[:, n:])  # padding untouched
+
+
+@pytest.mark.parametrize("algo", [SIMT, TF32X3])
+def test_degenerate_dims(algo):
+    """k = 1, n = 1 (tensor-core path with padded ld), m = 1; tall-skinny."""
+    for (m, n, k) in [(300, 4, 1), (1, 4, 64), (257, 1, 300), (5000, 8, 32)]:
+        pad = lambda x: (x + 3) // 4 * 4
+        lda, ldb, ldc = (pad(k), pad(n), pad(n)) if algo == TF32X3 else (k, n, n)
+        A, B, C0 = si.matrices(m, n, k, seed=m + k, lda=lda, ldb=ldb, ldc=ldc)
+        C, _ = run(A, B, C0, si.ALPHA, si.BETA, algo, lda=lda, ldb=ldb, ldc=ldc)
+        assert max_err(C, A, B, C0, si.ALPHA, si.BETA) <= TOL, (m, n, k)
+
+
+def test_auto_offsets_and_views():
+    """AUTO with torch views at element offsets: 16-B aligned sub-views take
+    the tensor-core path, misaligned ones fall back to SIMT; both correct."""
+    import torch
+    import paper_1804_10694_b200 as tm
+    m, n, k = 300, 200, 260
+    A, B, C0 = si.matrices(m + 4, n + 4, k + 4, seed=99)  # leading dims multiples of 4
+    dA, dB, dC = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (A, B, C0))
+    assert dA.stride(0) % 4 == 0 and dB.stride(0) % 4 == 0
+    for off in (0, 1, 4):
+        Av, Bv, Cv = dA[off:off + m - 1, off:off + k - 1], dB[off:off + k - 1, off:off + n - 1], dC.clone()[off:off + m - 1, off:off + n - 1]
+        Cref = Cv.cpu().numpy().copy()
+        path = tm.plan_name(m - 1, n - 1, k - 1, si.ALPHA, si.BETA, Av.data_ptr(), Av.stride(0), Bv.data_ptr(),
+                            Bv.stride(0), Cv.data_ptr(), Cv.stride(0))
+        assert path == ("simt" if off % 4 else "tf32x3"), (off, path)
+        tm.sgemm(Av, Bv, Cv, si.ALPHA, si.BETA)
+        torch.cuda.synchronize()
+        An, Bn = Av.cpu().numpy(), Bv.cpu().numpy()
+        assert max_err(Cv.cpu().numpy(), An, Bn, Cref, si.ALPHA, si.BETA) <= TOL, off
