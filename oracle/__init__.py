@@ -51,6 +51,9 @@ def _load():
         lib.tm_oracle_sgemm_rows.argtypes = [i64, i64, i64, f32, vp, i64, vp, i64,
                                              f32, vp, i64, i64, vp, vp, vp, i64]
         lib.tm_oracle_sgemm_rows.restype = ctypes.c_int
+        lib.tm_oracle_sgemm_op_rows.argtypes = [ctypes.c_int, ctypes.c_int, i64, i64, i64, f32, vp, i64, vp, i64,
+                                                f32, vp, i64, i64, vp, vp, vp, i64]
+        lib.tm_oracle_sgemm_op_rows.restype = ctypes.c_int
         lib.tm_oracle_sgemm_f64.argtypes = [i64, i64, i64, f32, vp, i64, vp, i64,
                                             f32, vp, i64, vp, vp, i64]
         lib.tm_oracle_sgemm_f64.restype = ctypes.c_int
@@ -83,25 +86,28 @@ def _ld(a):
     return max(a.shape[1], 1)
 
 
-def sgemm(alpha, A, B, beta, C0, rows=None, m=None, n=None, k=None):
-    """R, D for ``C = alpha*A@B + beta*C0`` (fp64), optionally only ``rows``.
+def sgemm(alpha, A, B, beta, C0, rows=None, m=None, n=None, k=None, opa="N", opb="N"):
+    """R, D for ``C = alpha*op(A)@op(B) + beta*C0`` (fp64), optionally only ``rows``.
 
-    A: m x k, B: k x n, C0: m x n float32 row-major views (any leading
-    dimension).  A/B may be None when alpha == 0 or k == 0, C0 may be None when
-    beta == 0 (they are then not read, reading 5).  Returns (R, D) as float64
-    arrays of shape (len(rows) or m, n).
+    op(X) = X for "N", X.T for "T" (as stored: A is m x k for "N", k x m for
+    "T"; B is k x n for "N", n x k for "T").  Float32 row-major views with any
+    leading dimension.  A/B may be None when alpha == 0 or k == 0, C0 may be
+    None when beta == 0 (they are then not read, reading 5).  Returns (R, D) as
+    float64 arrays of shape (len(rows) or m, n).
     """
     A = _check_f32("A", A)
     B = _check_f32("B", B)
     C0 = _check_f32("C0", C0)
+    ta, tb = int(opa == "T"), int(opb == "T")
     if m is None:
-        m = A.shape[0] if A is not None else C0.shape[0]
+        m = (A.shape[1] if ta else A.shape[0]) if A is not None else C0.shape[0]
     if k is None:
-        k = A.shape[1] if A is not None else (B.shape[0] if B is not None else 0)
+        k = (A.shape[0] if ta else A.shape[1]) if A is not None else (
+            (B.shape[1] if tb else B.shape[0]) if B is not None else 0)
     if n is None:
-        n = B.shape[1] if B is not None else C0.shape[1]
-    lda = _ld(A) if A is not None else max(k, 1)
-    ldb = _ld(B) if B is not None else max(n, 1)
+        n = (B.shape[0] if tb else B.shape[1]) if B is not None else C0.shape[1]
+    lda = _ld(A) if A is not None else max(m if ta else k, 1)
+    ldb = _ld(B) if B is not None else max(k if tb else n, 1)
     ldc = _ld(C0) if C0 is not None else max(n, 1)
     if rows is None:
         nrows, rows_arr = m, None
@@ -110,9 +116,9 @@ def sgemm(alpha, A, B, beta, C0, rows=None, m=None, n=None, k=None):
         nrows = rows_arr.shape[0]
     R = np.empty((nrows, n), dtype=np.float64)
     D = np.empty((nrows, n), dtype=np.float64)
-    rc = _load().tm_oracle_sgemm_rows(m, n, k, float(alpha), _ptr(A), lda, _ptr(B), ldb,
-                                      float(beta), _ptr(C0), ldc, nrows, _ptr(rows_arr),
-                                      _ptr(R), _ptr(D), max(n, 1))
+    rc = _load().tm_oracle_sgemm_op_rows(ta, tb, m, n, k, float(alpha), _ptr(A), lda, _ptr(B), ldb,
+                                         float(beta), _ptr(C0), ldc, nrows, _ptr(rows_arr),
+                                         _ptr(R), _ptr(D), max(n, 1))
     if rc != 0:
         raise ValueError(f"tm_oracle_sgemm_rows rejected its arguments (rc={rc})")
     return R, D

@@ -20,8 +20,11 @@
  *     err[i,j] = |C_gpu[i,j] - R[i,j]| / D[i,j]  <= 1e-5.
  *
  * Readings of points the paper leaves open:
- *   - storage is row-major, no transposes (reading 1, 2):
- *       A[i*lda+p], B[p*ldb+j], C0[i*ldc+j];
+ *   - storage is row-major (reading 1): A[i*lda+p], B[p*ldb+j], C0[i*ldc+j];
+ *   - transposed operands (BLAS op(A), op(B), not in the
+ *     paper, whose gemm has none, reading 2) only change WHERE element (i,p) of
+ *     A and (p,j) of B are read: opA = T reads A[p*lda+i], opB = T reads
+ *     B[j*ldb+p]; the products and their summation order are unchanged;
  *   - special cases follow reference-BLAS semantics (reading 5):
  *       beta == 0          -> C0 is NOT read (NaN in C0 does not propagate);
  *       alpha == 0 or k==0 -> A and B are NOT read, R = beta*C0;
@@ -54,15 +57,18 @@
 #include <omp.h>
 #endif
 
-static int check_args(int64_t m, int64_t n, int64_t k, float alpha,
+static int64_t max1(int64_t x) { return x > 1 ? x : 1; }
+
+static int check_args(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha,
                       const float *A, int64_t lda, const float *B, int64_t ldb,
                       float beta, const float *C0, int64_t ldc) {
     if (m < 0 || n < 0 || k < 0) return -1;
+    if ((opa != 0 && opa != 1) || (opb != 0 && opb != 1)) return -1;
     int reads_ab = (alpha != 0.0f) && (k > 0);
     if (reads_ab) {
         if (!A || !B) return -1;
-        if (lda < (k > 1 ? k : 1)) return -1;
-        if (ldb < (n > 1 ? n : 1)) return -1;
+        if (lda < (opa ? max1(m) : max1(k))) return -1;
+        if (ldb < (opb ? max1(k) : max1(n))) return -1;
     }
     if (beta != 0.0f) {
         if (!C0) return -1;
@@ -73,7 +79,7 @@ static int check_args(int64_t m, int64_t n, int64_t k, float alpha,
 
 /* One output row i of the definition above, into R_row[0..n), D_row[0..n).
  * acc/acc_abs are caller-provided scratch of n doubles each. */
-static void oracle_row(int64_t i, int64_t n, int64_t k, float alpha,
+static void oracle_row(int opa, int opb, int64_t i, int64_t n, int64_t k, float alpha,
                        const float *A, int64_t lda, const float *B, int64_t ldb,
                        float beta, const float *C0, int64_t ldc,
                        double *R_row, double *D_row, double *acc, double *acc_abs) {
@@ -82,11 +88,10 @@ static void oracle_row(int64_t i, int64_t n, int64_t k, float alpha,
     for (int64_t j = 0; j < n; ++j) { acc[j] = 0.0; acc_abs[j] = 0.0; }
     if (alpha != 0.0f) {
         for (int64_t p = 0; p < k; ++p) {
-            const double a = (double)A[i * lda + p];
+            const double a = (double)(opa ? A[p * lda + i] : A[i * lda + p]);   /* op(A)[i,p] */
             const double a_abs = fabs(a);
-            const float *Bp = B + p * ldb;
             for (int64_t j = 0; j < n; ++j) {
-                const double b = (double)Bp[j];
+                const double b = (double)(opb ? B[j * ldb + p] : B[p * ldb + j]); /* op(B)[p,j] */
                 acc[j] += a * b;             /* exact product, fp64 sum, p ascending */
                 acc_abs[j] += a_abs * fabs(b);
             }
@@ -108,15 +113,16 @@ static void oracle_row(int64_t i, int64_t n, int64_t k, float alpha,
     }
 }
 
-/* Rows rows[0..nrows) of R and D (row t of the outputs is row rows[t] of C);
- * rows == NULL means all rows 0..m-1 (nrows must then equal m).
- * R, D are nrows x n, row-major with leading dimension ldr >= n. */
-int tm_oracle_sgemm_rows(int64_t m, int64_t n, int64_t k, float alpha,
-                         const float *A, int64_t lda, const float *B, int64_t ldb,
-                         float beta, const float *C0, int64_t ldc,
-                         int64_t nrows, const int64_t *rows,
-                         double *R, double *D, int64_t ldr) {
-    if (check_args(m, n, k, alpha, A, lda, B, ldb, beta, C0, ldc)) return -1;
+/* Rows rows[0..nrows) of R and D for C = alpha*op(A)*op(B) + beta*C0 (row t of
+ * the outputs is row rows[t] of C); opa/opb: 0 = N, 1 = T.  rows == NULL means
+ * all rows 0..m-1 (nrows must then equal m).  R, D are nrows x n, row-major
+ * with leading dimension ldr >= n. */
+int tm_oracle_sgemm_op_rows(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha,
+                            const float *A, int64_t lda, const float *B, int64_t ldb,
+                            float beta, const float *C0, int64_t ldc,
+                            int64_t nrows, const int64_t *rows,
+                            double *R, double *D, int64_t ldr) {
+    if (check_args(opa, opb, m, n, k, alpha, A, lda, B, ldb, beta, C0, ldc)) return -1;
     if (nrows < 0 || ldr < n || (nrows > 0 && (!R || !D))) return -1;
     if (!rows && nrows != m) return -1;
     if (rows)
@@ -136,7 +142,7 @@ int tm_oracle_sgemm_rows(int64_t m, int64_t n, int64_t k, float alpha,
 #pragma omp for schedule(static)
             for (int64_t t = 0; t < nrows; ++t) {
                 const int64_t i = rows ? rows[t] : t;
-                oracle_row(i, n, k, alpha, A, lda, B, ldb, beta, C0, ldc,
+                oracle_row(opa, opb, i, n, k, alpha, A, lda, B, ldb, beta, C0, ldc,
                            R + t * ldr, D + t * ldr, acc, acc_abs);
             }
         }
@@ -144,6 +150,16 @@ int tm_oracle_sgemm_rows(int64_t m, int64_t n, int64_t k, float alpha,
         free(acc_abs);
     }
     return failed ? -2 : 0;
+}
+
+/* No transposes (the paper's gemm). */
+int tm_oracle_sgemm_rows(int64_t m, int64_t n, int64_t k, float alpha,
+                         const float *A, int64_t lda, const float *B, int64_t ldb,
+                         float beta, const float *C0, int64_t ldc,
+                         int64_t nrows, const int64_t *rows,
+                         double *R, double *D, int64_t ldr) {
+    return tm_oracle_sgemm_op_rows(0, 0, m, n, k, alpha, A, lda, B, ldb, beta, C0, ldc,
+                                   nrows, rows, R, D, ldr);
 }
 
 /* All rows: R, D are m x n with leading dimension ldr. */

@@ -248,3 +248,35 @@ def test_pins_catch_mutations():
     }
     for name, mut in mutants.items():
         assert np.max(np.abs(mut - good) / D) > 1e-3, name
+
+
+@pytest.mark.parametrize("opa,opb", [("N", "T"), ("T", "N"), ("T", "T")])
+def test_transposed_operands_pins(opa, opb):
+    """op(A), op(B) only change where elements are read: the oracle on
+    transposed storage must equal the NN oracle on explicit transposed copies
+    bit for bit (same products, same summation order), and exact rationals on
+    tiny shapes."""
+    m, n, k = 37, 23, 29
+    A, B, C0 = si.matrices(m, n, k, seed=71)
+    At = np.ascontiguousarray(A.T) if opa == "T" else A
+    Bt = np.ascontiguousarray(B.T) if opb == "T" else B
+    R0, D0 = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0)
+    R1, D1 = oracle.sgemm(si.ALPHA, At, Bt, si.BETA, C0, opa=opa, opb=opb)
+    assert np.array_equal(R0, R1) and np.array_equal(D0, D1)
+    # padded leading dimensions on the transposed storage
+    Ap = np.zeros((At.shape[0], At.shape[1] + 5), np.float32)
+    Ap[:, :At.shape[1]] = At
+    Bp = np.zeros((Bt.shape[0], Bt.shape[1] + 3), np.float32)
+    Bp[:, :Bt.shape[1]] = Bt
+    R2, _ = oracle.sgemm(si.ALPHA, Ap[:, :At.shape[1]], Bp[:, :Bt.shape[1]], si.BETA, C0, opa=opa, opb=opb)
+    assert np.array_equal(R0, R2)
+    g = si.rng(72)
+    for (mm, nn, kk) in [(2, 3, 4), (3, 1, 2), (1, 4, 3)]:
+        a, b, c = si.uniform(g, (mm, kk)), si.uniform(g, (kk, nn)), si.uniform(g, (mm, nn))
+        at = np.ascontiguousarray(a.T) if opa == "T" else a
+        bt = np.ascontiguousarray(b.T) if opb == "T" else b
+        R, _ = oracle.sgemm(1.5, at, bt, -0.75, c, opa=opa, opb=opb)
+        Rx, Dx = _exact(1.5, a, b, -0.75, c)
+        for i in range(mm):
+            for j in range(nn):
+                assert abs(Fraction(R[i, j]) - Rx[i][j]) <= Fraction((kk + 3) * EPS53 * float(Dx[i][j]))
