@@ -90,6 +90,27 @@ tm_status tm_sgemm_ex(int64_t m, int64_t n, int64_t k, float alpha,
                       const float* A, int64_t lda, const float* B, int64_t ldb,
                       float beta, float* C, int64_t ldc, void* stream, int algo);
 
+/* Transposed operands (BLAS op(); SURVEY.md 8(f) item 1 -- the paper's gemm,
+ * PAPER.md:67, has none).  Row-major storage throughout:
+ *   opa == TM_OP_N: A is m x k (lda >= max(1,k)), op(A)[i,p] = A[i*lda + p]
+ *   opa == TM_OP_T: A is k x m (lda >= max(1,m)), op(A)[i,p] = A[p*lda + i]
+ *   opb == TM_OP_N: B is k x n (ldb >= max(1,n)), op(B)[p,j] = B[p*ldb + j]
+ *   opb == TM_OP_T: B is n x k (ldb >= max(1,k)), op(B)[p,j] = B[j*ldb + p]
+ * C = alpha*op(A)*op(B) + beta*C, C m x n (ldc).  Same paths, accuracy, special
+ * cases and errors as tm_sgemm_ex (TM_ALGO_TF32X1 only for N,N). */
+typedef enum { TM_OP_N = 0, TM_OP_T = 1 } tm_op;
+tm_status tm_sgemm_op(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha,
+                      const float* A, int64_t lda, const float* B, int64_t ldb,
+                      float beta, float* C, int64_t ldc, void* stream, int algo);
+
+/* Reference-BLAS (column-major) sgemm: C = alpha*op(A)*op(B) + beta*C with
+ * transa/transb in {'N','T','C'} ('C' == 'T' for real data), A, B, C
+ * column-major with leading dimensions lda, ldb, ldc as in BLAS.  Implemented
+ * as the row-major product C^T = op(B)^T op(A)^T (no data movement). */
+tm_status tm_sgemm_colmajor(char transa, char transb, int64_t m, int64_t n, int64_t k, float alpha,
+                            const float* A, int64_t lda, const float* B, int64_t ldb,
+                            float beta, float* C, int64_t ldc, void* stream);
+
 /* End-to-end entry with HOST buffers (ideally pinned): copies A, B (and C when
  * beta != 0) to the current device, computes, copies C back, and synchronises
  * `stream` before returning.  Host->device copies of row blocks of A/C overlap

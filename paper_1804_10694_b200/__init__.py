@@ -25,7 +25,7 @@ lib_path = os.path.join(_PKG, "_lib", "libtm.so")
 
 # Every function include/tm.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = [
-    "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
+    "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_op", "tm_sgemm_colmajor", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
     "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
     "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_bytes_received",
 ]
@@ -48,6 +48,8 @@ def _load():
     L.tm_sgemm.argtypes = gemm
     L.tm_sgemm_ex.argtypes = gemm + [ci]
     L.tm_sgemm_host.argtypes = gemm + [ci]
+    L.tm_sgemm_op.argtypes = [ci, ci] + gemm + [ci]
+    L.tm_sgemm_colmajor.argtypes = [ctypes.c_char, ctypes.c_char] + gemm
     L.tm_sgemm_plan_name.argtypes = [i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, ci]
     L.tm_sgemm_plan_name.restype = ctypes.c_char_p
     L.tm_status_string.argtypes = [ci]
@@ -137,6 +139,20 @@ def sgemm_ex(A, B, C, alpha: float = 1.0, beta: float = 0.0, algo: int = ALGO_AU
     st = lib.tm_sgemm_ex(m, n, k, float(alpha), _ptr(A), lda, _ptr(B), ldb, float(beta), _ptr(C), _ld(C),
                          _stream(stream), int(algo))
     _check(st, "tm_sgemm_ex")
+    return C
+
+
+def sgemm_op(A, B, C, alpha: float = 1.0, beta: float = 0.0, opa: str = "N", opb: str = "N",
+             algo: int = ALGO_AUTO, stream=None):
+    """C <- alpha*op(A)@op(B) + beta*C; A, B given as stored (A is k x m when
+    opa == "T", B is n x k when opb == "T"), row-major CUDA tensors."""
+    A, B, C = _f32("A", A), _f32("B", B), _f32("C", C)
+    m, n = C.shape
+    ta, tb = opa == "T", opb == "T"
+    k = A.shape[0] if ta else A.shape[1]
+    st = lib.tm_sgemm_op(int(ta), int(tb), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B), float(beta),
+                         _ptr(C), _ld(C), _stream(stream), int(algo))
+    _check(st, "tm_sgemm_op")
     return C
 
 

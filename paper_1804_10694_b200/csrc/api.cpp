@@ -92,11 +92,12 @@ Plan make_plan(const GemmArgs& a, int algo, int num_sms) {
     pl.path = Path::kScale;
     return pl;
   }
-  if (!a.A || !a.B || a.lda < kk || a.ldb < nn) return pl;
+  const int64_t mm = a.m > 1 ? a.m : 1;
+  if (!a.A || !a.B || a.lda < (a.ta ? mm : kk) || a.ldb < (a.tb ? kk : nn)) return pl;
   const int64_t cbytes = extent_bytes(a.m, a.n, a.ldc);
-  if (ranges_overlap(a.C, cbytes, a.A, extent_bytes(a.m, a.k, a.lda)) ||
-      ranges_overlap(a.C, cbytes, a.B, extent_bytes(a.k, a.n, a.ldb)))
-    return pl;
+  const int64_t abytes = a.ta ? extent_bytes(a.k, a.m, a.lda) : extent_bytes(a.m, a.k, a.lda);
+  const int64_t bbytes = a.tb ? extent_bytes(a.n, a.k, a.ldb) : extent_bytes(a.k, a.n, a.ldb);
+  if (ranges_overlap(a.C, cbytes, a.A, abytes) || ranges_overlap(a.C, cbytes, a.B, bbytes)) return pl;
   const bool aligned = tc_aligned(a);
   switch (algo) {
     case TM_ALGO_SIMT_F32:
@@ -273,6 +274,32 @@ tm_status tm_sgemm_ex(int64_t m, int64_t n, int64_t k, float alpha, const float*
 tm_status tm_sgemm(int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda, const float* B,
                    int64_t ldb, float beta, float* C, int64_t ldc, void* stream) {
   return tm_sgemm_ex(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, stream, TM_ALGO_AUTO);
+}
+
+tm_status tm_sgemm_op(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda,
+                      const float* B, int64_t ldb, float beta, float* C, int64_t ldc, void* stream, int algo) {
+  if ((opa != TM_OP_N && opa != TM_OP_T) || (opb != TM_OP_N && opb != TM_OP_T)) return TM_ERR_INVALID_VALUE;
+  if (algo == TM_ALGO_TF32X1 && (opa != TM_OP_N || opb != TM_OP_N)) return TM_ERR_INVALID_VALUE;
+  GemmArgs a{m, n, k, alpha, beta, A, lda, B, ldb, C, ldc, opa == TM_OP_T, opb == TM_OP_T};
+  try {
+    return tmk::run(a, algo, static_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return TM_ERR_INTERNAL;
+  }
+}
+
+// Column-major BLAS convention: C (m x n, ldc) = alpha op(A) op(B) + beta C.
+// Its memory is the row-major matrix C^T (n x m) = op(B)^T op(A)^T, and a
+// column-major operand is a row-major operand transposed, so this is the
+// row-major product with operands swapped and the same trans flags:
+//   rowmajor(op_x = transb, op_y = transa, m' = n, n' = m, X = B, Y = A).
+tm_status tm_sgemm_colmajor(char transa, char transb, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
+                            int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc,
+                            void* stream) {
+  auto op = [](char t) { return (t == 'N' || t == 'n') ? TM_OP_N : (t == 'T' || t == 't' || t == 'C' || t == 'c') ? TM_OP_T : -1; };
+  const int ta = op(transa), tb = op(transb);
+  if (ta < 0 || tb < 0) return TM_ERR_INVALID_VALUE;
+  return tm_sgemm_op(tb, ta, n, m, k, alpha, B, ldb, A, lda, beta, C, ldc, stream, TM_ALGO_AUTO);
 }
 
 const char* tm_sgemm_plan_name(int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda,

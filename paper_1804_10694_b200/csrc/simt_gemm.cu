@@ -1,7 +1,8 @@
 // simt_gemm.cu -- pure-FP32 SIMT sgemm (validation path) and the C = beta*C
 // special-case kernel.
 //
-// C = alpha*A*B + beta*C with FFMA accumulation in fp32.
+// C = alpha*op(A)*op(B) + beta*C (op = transposes)
+// with FFMA accumulation in fp32.
 // The paper's GPU gemm optimisations: two-level tiling (CTA
 // tile 128x128, per-thread 8x8 register block -- "register blocking"),
 // shared-memory staging with double buffering ("data movement between global,
@@ -34,31 +35,22 @@ struct SimtParams {
   bool vec_c;  // C 16-B aligned and ldc % 4 == 0
 };
 
+// 4 consecutive elements [inner, inner+4) of row `outer` of a row-major array
+// (leading dimension ld), zero outside [0, outer_lim) x [0, inner_lim).
 template <bool VEC>
-__device__ __forceinline__ void load_a(const SimtParams& p, int64_t row, int64_t kq, float (&v)[4]) {
-  // 4 consecutive k of one row of A
-  if (VEC && row < p.m && kq + 3 < p.k) {
-    const float4 t = __ldg(reinterpret_cast<const float4*>(p.A + row * p.lda + kq));
+__device__ __forceinline__ void load4(const float* __restrict__ X, int64_t ld, int64_t outer, int64_t outer_lim,
+                                      int64_t inner, int64_t inner_lim, float (&v)[4]) {
+  if (VEC && outer < outer_lim && inner + 3 < inner_lim) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(X + outer * ld + inner));
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = (row < p.m && kq + i < p.k) ? __ldg(p.A + row * p.lda + kq + i) : 0.0f;
+    for (int i = 0; i < 4; ++i) v[i] = (outer < outer_lim && inner + i < inner_lim) ? __ldg(X + outer * ld + inner + i) : 0.0f;
   }
 }
 
-template <bool VEC>
-__device__ __forceinline__ void load_b(const SimtParams& p, int64_t krow, int64_t col, float (&v)[4]) {
-  // 4 consecutive columns of one row of B
-  if (VEC && krow < p.k && col + 3 < p.n) {
-    const float4 t = __ldg(reinterpret_cast<const float4*>(p.B + krow * p.ldb + col));
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = (krow < p.k && col + i < p.n) ? __ldg(p.B + krow * p.ldb + col + i) : 0.0f;
-  }
-}
-
-template <bool VEC>
+// TA: op(A) = A^T (A stored k x m); TB: op(B) = B^T (B stored n x k).
+template <bool VEC, bool TA, bool TB>
 __global__ void __launch_bounds__(STHREADS, 2) k_sgemm_simt(SimtParams p) {
   __shared__ __align__(16) float As[2][SBK][SBM + 4];  // k-major copy of the A tile
   __shared__ __align__(16) float Bs[2][SBK][SBN];
@@ -68,17 +60,39 @@ __global__ void __launch_bounds__(STHREADS, 2) k_sgemm_simt(SimtParams p) {
   const int64_t bm = blockIdx.x / p.tiles_n, bn = blockIdx.x % p.tiles_n;
   const int64_t row0 = bm * SBM, col0 = bn * SBN;
 
-  const int a_r = tid >> 1, a_k = (tid & 1) * 4;   // A: 128 rows x 8 k
-  const int b_k = tid >> 5, b_c = (tid & 31) * 4;  // B: 8 k x 128 cols
+  // Global -> register mapping (each thread loads 4 contiguous elements):
+  //   A  (m x k, K contiguous):  row tid/2,        k (tid%2)*4..+3   -> transposed smem stores
+  //   A^T(k x m, M contiguous):  k tid/32,         rows (tid%32)*4   -> one 16-B smem store
+  //   B  (k x n, N contiguous):  k tid/32,         cols (tid%32)*4   -> one 16-B smem store
+  //   B^T(n x k, K contiguous):  col tid/2,        k (tid%2)*4..+3   -> transposed smem stores
+  const int a_o = TA ? (tid >> 5) : (tid >> 1), a_i = TA ? (tid & 31) * 4 : (tid & 1) * 4;
+  const int b_o = TB ? (tid >> 1) : (tid >> 5), b_i = TB ? (tid & 1) * 4 : (tid & 31) * 4;
 
   float ar[4], br[4];
   const int64_t nk = (p.k + SBK - 1) / SBK;
-
-  load_a<VEC>(p, row0 + a_r, a_k, ar);
-  load_b<VEC>(p, b_k, col0 + b_c, br);
+  auto load_tiles = [&](int64_t k0) {
+    if (TA) load4<VEC>(p.A, p.lda, k0 + a_o, p.k, row0 + a_i, p.m, ar);
+    else load4<VEC>(p.A, p.lda, row0 + a_o, p.m, k0 + a_i, p.k, ar);
+    if (TB) load4<VEC>(p.B, p.ldb, col0 + b_o, p.n, k0 + b_i, p.k, br);
+    else load4<VEC>(p.B, p.ldb, k0 + b_o, p.k, col0 + b_i, p.n, br);
+  };
+  auto store_tiles = [&](int buf) {
+    if (TA) {
+      *reinterpret_cast<float4*>(&As[buf][a_o][a_i]) = make_float4(ar[0], ar[1], ar[2], ar[3]);
+    } else {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) As[0][a_k + i][a_r] = ar[i];
-  *reinterpret_cast<float4*>(&Bs[0][b_k][b_c]) = make_float4(br[0], br[1], br[2], br[3]);
+      for (int i = 0; i < 4; ++i) As[buf][a_i + i][a_o] = ar[i];
+    }
+    if (TB) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) Bs[buf][b_i + i][b_o] = br[i];
+    } else {
+      *reinterpret_cast<float4*>(&Bs[buf][b_o][b_i]) = make_float4(br[0], br[1], br[2], br[3]);
+    }
+  };
+
+  load_tiles(0);
+  store_tiles(0);
   __syncthreads();
 
   float acc[8][8];
@@ -90,11 +104,7 @@ __global__ void __launch_bounds__(STHREADS, 2) k_sgemm_simt(SimtParams p) {
   for (int64_t kb = 0; kb < nk; ++kb) {
     const int cur = static_cast<int>(kb & 1);
     const bool more = kb + 1 < nk;
-    if (more) {  // prefetch the next K-block into registers while computing this one
-      const int64_t k0 = (kb + 1) * SBK;
-      load_a<VEC>(p, row0 + a_r, k0 + a_k, ar);
-      load_b<VEC>(p, k0 + b_k, col0 + b_c, br);
-    }
+    if (more) load_tiles((kb + 1) * SBK);  // prefetch the next K-block into registers while computing this one
 #pragma unroll
     for (int kk = 0; kk < SBK; ++kk) {
       const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][kk][ty * 4]);
@@ -109,9 +119,7 @@ __global__ void __launch_bounds__(STHREADS, 2) k_sgemm_simt(SimtParams p) {
         for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
     if (more) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) As[cur ^ 1][a_k + i][a_r] = ar[i];
-      *reinterpret_cast<float4*>(&Bs[cur ^ 1][b_k][b_c]) = make_float4(br[0], br[1], br[2], br[3]);
+      store_tiles(cur ^ 1);
       __syncthreads();
     }
   }
@@ -174,10 +182,18 @@ tm_status launch_simt(const GemmArgs& a, cudaStream_t stream) {
   p.vec_c = (reinterpret_cast<uintptr_t>(a.C) % 16 == 0) && (a.ldc % 4 == 0);
   const bool vec = (reinterpret_cast<uintptr_t>(a.A) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.B) % 16 == 0) &&
                    (a.lda % 4 == 0) && (a.ldb % 4 == 0);
-  if (vec)
-    k_sgemm_simt<true><<<static_cast<unsigned>(tiles), STHREADS, 0, stream>>>(p);
-  else
-    k_sgemm_simt<false><<<static_cast<unsigned>(tiles), STHREADS, 0, stream>>>(p);
+  const unsigned g = static_cast<unsigned>(tiles);
+  const int v = (vec ? 4 : 0) | (a.ta ? 2 : 0) | (a.tb ? 1 : 0);
+  switch (v) {
+    case 0: k_sgemm_simt<false, false, false><<<g, STHREADS, 0, stream>>>(p); break;
+    case 1: k_sgemm_simt<false, false, true><<<g, STHREADS, 0, stream>>>(p); break;
+    case 2: k_sgemm_simt<false, true, false><<<g, STHREADS, 0, stream>>>(p); break;
+    case 3: k_sgemm_simt<false, true, true><<<g, STHREADS, 0, stream>>>(p); break;
+    case 4: k_sgemm_simt<true, false, false><<<g, STHREADS, 0, stream>>>(p); break;
+    case 5: k_sgemm_simt<true, false, true><<<g, STHREADS, 0, stream>>>(p); break;
+    case 6: k_sgemm_simt<true, true, false><<<g, STHREADS, 0, stream>>>(p); break;
+    default: k_sgemm_simt<true, true, true><<<g, STHREADS, 0, stream>>>(p); break;
+  }
   return cudaGetLastError() == cudaSuccess ? TM_OK : TM_ERR_CUDA;
 }
 

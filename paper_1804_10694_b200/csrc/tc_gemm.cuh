@@ -1,4 +1,6 @@
-// tc_gemm.cu -- 3xTF32 split-operand sgemm on the sm_100a tensor cores.
+// tc_gemm.cuh -- 3xTF32 split-operand sgemm on the sm_100a tensor cores
+// (kernel + host launch templates; instantiated per operand layout in
+// tc_gemm_{nn,nt,tn,tt}.cu so the four variants compile in parallel).
 //
 // Computes C = alpha*A*B + beta*C in fp32-faithful accuracy:
 // every fp32 operand x is split as x = hi + lo with hi = x truncated to TF32
@@ -34,6 +36,7 @@
 //               owns TMEM lanes 32*(w%4).. (rows) and column half (w-8)/4.
 // CG == 2 runs a CTA pair (cta_group::2): tile 256 x (2*BN_CTA), A split along
 // M and B along N between the two CTAs' shared memories; CTA 0 issues MMAs.
+#pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -271,7 +274,9 @@ __device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, 
   }
 }
 
-template <int CG, int BN_CTA, bool SPLIT3>
+// TA / TB: op(A) = A^T (A stored k x m, M contiguous -> MN-major A operand) /
+// op(B) = B^T (B stored n x k, K contiguous -> K-major B operand).
+template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
   using Cfg = TcCfg<CG, BN_CTA, SPLIT3>;
@@ -355,10 +360,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::mbar_wait(&empty_raw[s], ph ^ 1);
             ptx::mbar_arrive_expect_tx(&full[s], Cfg::kABytes + Cfg::kBBytes);
-            ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * kBK, row0);
+            if constexpr (!TA) {  // A: one K-major box 32 (k) x 128 (rows)
+              ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * kBK, row0);
+            } else {              // A^T: four MN-major boxes 32 (rows) x 32 (k)
 #pragma unroll
-            for (int j = 0; j < BN_CTA / 32; ++j)
-              ptx::tma_load_2d(rawB + s * Cfg::kBBytes + j * 4096, &tmB, &full[s], col0 + 32 * j, kb * kBK);
+              for (int j = 0; j < kBMCta / 32; ++j)
+                ptx::tma_load_2d(rawA + s * Cfg::kABytes + j * 4096, &tmA, &full[s], row0 + 32 * j, kb * kBK);
+            }
+            if constexpr (!TB) {  // B: BN_CTA/32 MN-major boxes 32 (cols) x 32 (k)
+#pragma unroll
+              for (int j = 0; j < BN_CTA / 32; ++j)
+                ptx::tma_load_2d(rawB + s * Cfg::kBBytes + j * 4096, &tmB, &full[s], col0 + 32 * j, kb * kBK);
+            } else {              // B^T: one K-major box 32 (k) x BN_CTA (cols)
+              ptx::tma_load_2d(rawB + s * Cfg::kBBytes, &tmB, &full[s], kb * kBK, col0);
+            }
             if (++s == RAW) { s = 0; ph ^= 1; }
           }
         }
@@ -367,7 +382,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
       if (rank == 0 && ptx::elect_one()) {
-        constexpr uint32_t idesc = ptx::idesc_tf32(Cfg::kMmaM, Cfg::kMmaN, /*A MN-major*/ 0, /*B MN-major*/ 1);
+        constexpr uint32_t idesc = ptx::idesc_tf32(Cfg::kMmaM, Cfg::kMmaN, /*A MN-major*/ TA ? 1 : 0,
+                                                   /*B MN-major*/ TB ? 0 : 1);
+        // K-major tile (rows of 128 B = 32 k, SWIZZLE_128B): K step of 8 = 32 B inside the row.
+        // MN-major tile (rows of 128 B = 32 m/n, 32-B-atom swizzle): K step of 8 rows = 1024 B
+        // (two 512-B atoms, SBO); 32-column atoms 4096 B apart (LBO).
+        auto desc_k = [](uint32_t base, int ks) { return ptx::sdesc(base + ks * 32, 16, 1024, ptx::kLayoutSW128); };
+        auto desc_mn = [](uint32_t base, int ks) {
+          return ptx::sdesc(base + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
+        };
         const uint32_t rawA_s = ptx::smem_u32(rawA), rawB_s = ptx::smem_u32(rawB);
         const uint32_t loA_s = ptx::smem_u32(loA), loB_s = ptx::smem_u32(loB);
         int s = 0, sl = 0, pb = 0;
@@ -386,17 +409,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (kb == 0 && s == 0 && ph == 0) trace_mark(p, 4);  // first MMA issue
 #pragma unroll
               for (int ks = 0; ks < kBK / 8; ++ks) {
-                // A: K-major SW128, K step of 8 tf32 = 32 B inside the swizzle row.
-                // B: MN-major SW128_BASE32B, K step of 8 rows = 1024 B (two 512-B
-                //    atoms, SBO); 32-column atoms are 4096 B apart (LBO).
-                const uint64_t aH = ptx::sdesc(rawA_s + s * Cfg::kABytes + ks * 32, 16, 1024, ptx::kLayoutSW128);
-                const uint64_t bH =
-                    ptx::sdesc(rawB_s + s * Cfg::kBBytes + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
+                const uint64_t aH = TA ? desc_mn(rawA_s + s * Cfg::kABytes, ks) : desc_k(rawA_s + s * Cfg::kABytes, ks);
+                const uint64_t bH = TB ? desc_k(rawB_s + s * Cfg::kBBytes, ks) : desc_mn(rawB_s + s * Cfg::kBBytes, ks);
                 const uint32_t acc = (kb != kb0 || ks != 0) ? 1u : 0u;  // fresh partial per K_c chunk
                 if constexpr (SPLIT3) {
-                  const uint64_t aL = ptx::sdesc(loA_s + sl * Cfg::kABytes + ks * 32, 16, 1024, ptx::kLayoutSW128);
-                  const uint64_t bL =
-                      ptx::sdesc(loB_s + sl * Cfg::kBBytes + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
+                  const uint64_t aL = TA ? desc_mn(loA_s + sl * Cfg::kABytes, ks) : desc_k(loA_s + sl * Cfg::kABytes, ks);
+                  const uint64_t bL = TB ? desc_k(loB_s + sl * Cfg::kBBytes, ks) : desc_mn(loB_s + sl * Cfg::kBBytes, ks);
                   // A_hi feeds two MMAs back to back: fetched from smem once (collector fill/lastuse)
                   ptx::mma_tf32<CG>(d, aL, bH, idesc, acc);
                   ptx::mma_tf32<CG, 1>(d, aH, bL, idesc, 1u);
@@ -586,10 +604,10 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, 
   return r == CUDA_SUCCESS;
 }
 
-template <int CG, int BN_CTA, bool SPLIT3>
+template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB>
 tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t stream) {
   using Cfg = TcCfg<CG, BN_CTA, SPLIT3>;
-  auto kern = k_sgemm_tc<CG, BN_CTA, SPLIT3>;
+  auto kern = k_sgemm_tc<CG, BN_CTA, SPLIT3, TA, TB>;
   static bool attr_set = false;  // per instantiation; attribute is per-function, process-wide
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes) != cudaSuccess)
@@ -597,9 +615,15 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t 
     attr_set = true;
   }
   CUtensorMap tmA, tmB;
-  // A: m x k, box 32 (k) x 128 (rows).  B: k x n, box 32 (n) x 32 (k rows).
-  if (!encode_2d(&tmA, a.A, a.m, a.k, a.lda, kBK, kBMCta, CU_TENSOR_MAP_SWIZZLE_128B)) return TM_ERR_INTERNAL;
-  if (!encode_2d(&tmB, a.B, a.k, a.n, a.ldb, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return TM_ERR_INTERNAL;
+  // K-major operands (A, B^T): box 32 (k) x rows, SWIZZLE_128B.  MN-major
+  // operands (A^T, B): box 32 (m or n) x 32 (k), 128-B swizzle with 32-B atoms.
+  bool ok;
+  if constexpr (!TA) ok = encode_2d(&tmA, a.A, a.m, a.k, a.lda, kBK, kBMCta, CU_TENSOR_MAP_SWIZZLE_128B);
+  else ok = encode_2d(&tmA, a.A, a.k, a.m, a.lda, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (!ok) return TM_ERR_INTERNAL;
+  if constexpr (!TB) ok = encode_2d(&tmB, a.B, a.k, a.n, a.ldb, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  else ok = encode_2d(&tmB, a.B, a.n, a.k, a.ldb, kBK, BN_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!ok) return TM_ERR_INTERNAL;
   TcParams p;
   p.A = a.A;
   p.lda = a.lda;
@@ -673,26 +697,31 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t 
   return TM_OK;
 }
 
-template <bool SPLIT3>
+template <bool SPLIT3, bool TA, bool TB>
 tm_status launch_split(const GemmArgs& a, int cg, int bn, int num_sms, bool sk, cudaStream_t s) {
   if (cg == 2) {
-    if (bn == 128) return launch_cfg<2, 128, SPLIT3>(a, num_sms, sk, s);
-    if (bn == 64) return launch_cfg<2, 64, SPLIT3>(a, num_sms, sk, s);
-    if (bn == 32) return launch_cfg<2, 32, SPLIT3>(a, num_sms, sk, s);
+    if (bn == 128) return launch_cfg<2, 128, SPLIT3, TA, TB>(a, num_sms, sk, s);
+    if (bn == 64) return launch_cfg<2, 64, SPLIT3, TA, TB>(a, num_sms, sk, s);
+    if (bn == 32) return launch_cfg<2, 32, SPLIT3, TA, TB>(a, num_sms, sk, s);
   } else if (cg == 1) {
-    if (bn == 128) return launch_cfg<1, 128, SPLIT3>(a, num_sms, sk, s);
-    if (bn == 64) return launch_cfg<1, 64, SPLIT3>(a, num_sms, sk, s);
-    if (bn == 32) return launch_cfg<1, 32, SPLIT3>(a, num_sms, sk, s);
+    if (bn == 128) return launch_cfg<1, 128, SPLIT3, TA, TB>(a, num_sms, sk, s);
+    if (bn == 64) return launch_cfg<1, 64, SPLIT3, TA, TB>(a, num_sms, sk, s);
+    if (bn == 32) return launch_cfg<1, 32, SPLIT3, TA, TB>(a, num_sms, sk, s);
   }
   return TM_ERR_INVALID_VALUE;
 }
 
 }  // namespace
 
-tm_status launch_tc(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream) {
+// Tensor-core launch for one operand layout (explicitly instantiated in
+// tc_gemm_{nn,nt,tn,tt}.cu).  The single-pass TF32 bring-up mode exists only
+// for the NN layout.
+template <bool TA, bool TB>
+tm_status launch_tc_op(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream) {
   if (a.m > INT32_MAX / 2 || a.n > INT32_MAX / 2 || a.k > INT32_MAX / 2) return TM_ERR_INVALID_VALUE;
-  return c.split3 ? launch_split<true>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream)
-                  : launch_split<false>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
+  if (c.split3) return launch_split<true, TA, TB>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
+  if constexpr (!TA && !TB) return launch_split<false, false, false>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
+  return TM_ERR_INVALID_VALUE;
 }
 
 }  // namespace tmk

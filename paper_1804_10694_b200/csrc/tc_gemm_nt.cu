@@ -1,0 +1,6 @@
+// tc_gemm_nt.cu -- instantiates the 3xTF32 tensor-core GEMM for op(A) = A, op(B) = B^T.
+#include "tc_gemm.cuh"
+
+namespace tmk {
+template tm_status launch_tc_op<false, true>(const GemmArgs&, const TcChoice&, int, cudaStream_t);
+}  // namespace tmk

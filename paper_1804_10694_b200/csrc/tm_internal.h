@@ -8,6 +8,8 @@
 
 namespace tmk {
 
+// C = alpha * op(A) * op(B) + beta * C, row-major.  ta: op(A) = A^T (A stored
+// k x m, lda >= m); tb: op(B) = B^T (B stored n x k, ldb >= k).
 struct GemmArgs {
   int64_t m, n, k;
   float alpha, beta;
@@ -17,6 +19,7 @@ struct GemmArgs {
   int64_t ldb;
   float* C;
   int64_t ldc;
+  bool ta = false, tb = false;
 };
 
 // Tensor-core configuration: CTA group (1 or 2), B columns per CTA (32/64/128),
@@ -28,7 +31,14 @@ struct TcChoice {
   bool streamk;  // stream-K decomposition (wave-quantized shapes)
 };
 
-tm_status launch_tc(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream);
+template <bool TA, bool TB>
+tm_status launch_tc_op(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream);
+inline tm_status launch_tc(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream) {
+  if (!a.ta && !a.tb) return launch_tc_op<false, false>(a, c, num_sms, stream);
+  if (!a.ta && a.tb) return launch_tc_op<false, true>(a, c, num_sms, stream);
+  if (a.ta && !a.tb) return launch_tc_op<true, false>(a, c, num_sms, stream);
+  return launch_tc_op<true, true>(a, c, num_sms, stream);
+}
 tm_status launch_simt(const GemmArgs& a, cudaStream_t stream);
 tm_status launch_scale(int64_t m, int64_t n, float beta, float* C, int64_t ldc, cudaStream_t stream);
 

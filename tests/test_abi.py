@@ -121,3 +121,16 @@ def test_product_package_never_imports_oracle():
                 with open(os.path.join(dirpath, f)) as fh:
                     src = fh.read()
                 assert "oracle" not in src.replace("# no oracle", ""), f
+
+
+def test_op_and_colmajor_validation_on_host():
+    L = tm.lib
+    vp = ctypes.c_void_p
+    # opa = T: lda must be >= m
+    assert L.tm_sgemm_op(1, 0, 64, 8, 16, 1.0, vp(16), 32, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None, 0) == 1
+    # opb = T: ldb must be >= k
+    assert L.tm_sgemm_op(0, 1, 8, 64, 16, 1.0, vp(16), 16, vp(1 << 16), 8, 0.0, vp(1 << 24), 64, None, 0) == 1
+    assert L.tm_sgemm_op(2, 0, 8, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None, 0) == 1
+    assert L.tm_sgemm_op(1, 0, 8, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None, 3) == 1
+    assert L.tm_sgemm_colmajor(b"X", b"N", 8, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None) == 1
+    assert L.tm_sgemm_op(1, 1, 0, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None, 0) == 0  # noop
