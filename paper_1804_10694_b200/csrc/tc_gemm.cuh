@@ -698,9 +698,12 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t 
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   // Stream-K finalizers and the wave barrier wait on other CTAs: require the
-  // whole (persistent, <= one CTA per SM) grid to be co-resident.
+  // whole (persistent, <= one CTA per SM) grid to be co-resident.  Nsight
+  // Compute cannot replay cooperative cluster launches; TM_COOPERATIVE=0 drops
+  // only this launch-time check for profiling runs (same kernel, same barrier).
+  static const bool coop = [] { const char* e = std::getenv("TM_COOPERATIVE"); return !(e && e[0] == '0'); }();
   attr[1].id = cudaLaunchAttributeCooperative;
-  attr[1].val.cooperative = (p.streamk || p.wave_ctr) ? 1 : 0;
+  attr[1].val.cooperative = (coop && (p.streamk || p.wave_ctr)) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   p.trace = nullptr;
