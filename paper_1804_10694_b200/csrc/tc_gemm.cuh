@@ -283,6 +283,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
   using Cfg = TcCfg<CG, BN_CTA, SPLIT3>;
   constexpr int RAW = Cfg::kRaw, LO = Cfg::kLo, KCOLS = Cfg::kCols;
+  // A_lo staged in TMEM (written by the split warps with tcgen05.st, read by
+  // the A_lo*B_hi MMA directly from tensor memory): saves its shared-memory
+  // write and read.  Needs K-major A and free TMEM columns beyond the two
+  // partial accumulators (not the 2-CTA 256-column tile, whose partials use
+  // all 512 columns).
+  constexpr bool ALO = SPLIT3 && !TA && (2 * Cfg::kMmaN + LO * kBK <= 512);
+  constexpr int kTmemNeed = 2 * Cfg::kMmaN + (ALO ? LO * kBK : 0);
+  constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
+  constexpr uint32_t kAloCol = 2 * Cfg::kMmaN;  // first TMEM column of the A_lo stages
 
   extern __shared__ uint8_t smem_raw_[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw_) + 1023) & ~uintptr_t(1023));
@@ -326,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
   }
-  if (warp == 2) ptx::tmem_alloc<CG>(tmem_base_slot, Cfg::kTmemCols);
+  if (warp == 2) ptx::tmem_alloc<CG>(tmem_base_slot, kTmemCols);
   ptx::tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) ptx::cluster_sync();
@@ -335,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) trace_mark(p, 1);
 
   if (warp < 4) {
-    ptx::setmaxnreg_dec<72>();
+    ptx::setmaxnreg_dec<80>();  // producer / MMA / allocator warpgroup
     if (warp == 0) {
       // ---------------------------------------------------------- producer
       if (ptx::elect_one()) {
@@ -425,9 +434,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t acc = (kb != kb0 || ks != 0) ? 1u : 0u;  // fresh partial per K_c chunk
                 if constexpr (SPLIT3) {
                   const uint64_t aL = TA ? desc_mn(loA_s + sl * Cfg::kABytes, ks) : desc_k(loA_s + sl * Cfg::kABytes, ks);
+                  (void)aL;
                   const uint64_t bL = TB ? desc_k(loB_s + sl * Cfg::kBBytes, ks) : desc_mn(loB_s + sl * Cfg::kBBytes, ks);
                   // A_hi feeds two MMAs back to back: fetched from smem once (collector fill/lastuse)
-                  ptx::mma_tf32<CG>(d, aL, bH, idesc, acc);
+                  if constexpr (ALO) {
+                    constexpr uint32_t idesc_k = ptx::idesc_tf32(Cfg::kMmaM, Cfg::kMmaN, 0, TB ? 0 : 1);
+                    ptx::mma_tf32_tmem_a<CG>(d, tmem_base + kAloCol + sl * kBK + ks * 8, bH, idesc_k, acc);
+                  } else {
+                    ptx::mma_tf32<CG>(d, aL, bH, idesc, acc);
+                  }
                   ptx::mma_tf32<CG, 1>(d, aH, bL, idesc, 1u);
                   ptx::mma_tf32<CG, 2>(d, aH, bH, idesc, 1u);
                 } else {
@@ -448,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ split
-    ptx::setmaxnreg_dec<72>();
+    ptx::setmaxnreg_dec<64>();  // split warpgroup: (80 + 64) * 128 + 184 * 256 = 65536
     const int st = threadIdx.x - 128;
     const uint32_t rawA_s = ptx::smem_u32(rawA), rawB_s = ptx::smem_u32(rawB);
     const uint32_t loA_s = ptx::smem_u32(loA), loB_s = ptx::smem_u32(loB);
@@ -463,7 +478,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (an mbarrier phase may not complete twice before it is observed).
         ptx::mbar_wait(&empty_lo[sl], phl ^ 1);
         if constexpr (SPLIT3) {
-          split_tile<Cfg::kABytes>(rawA_s + s * Cfg::kABytes, loA_s + sl * Cfg::kABytes, st);
+          if constexpr (ALO) {
+            // Row r = this thread's TMEM lane (warp w owns lanes 32*(w%4)..+31):
+            // read its 128-B row of the raw K-major A tile (16-B chunk c lives
+            // at chunk c ^ (r % 8)), split, store 32 columns of A_lo.
+            const int r = st;
+            const uint32_t rowp = rawA_s + s * Cfg::kABytes + r * 128;
+            uint32_t lo[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint4 v = ptx::lds128(rowp + ((c ^ (r & 7)) << 4));
+              lo[4 * c] = tf32_lo_bits(v.x);
+              lo[4 * c + 1] = tf32_lo_bits(v.y);
+              lo[4 * c + 2] = tf32_lo_bits(v.z);
+              lo[4 * c + 3] = tf32_lo_bits(v.w);
+            }
+            ptx::tmem_st_32x32b_x32(tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + kAloCol + sl * kBK, lo);
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+          } else {
+            split_tile<Cfg::kABytes>(rawA_s + s * Cfg::kABytes, loA_s + sl * Cfg::kABytes, st);
+          }
           split_tile<Cfg::kBBytes>(rawB_s + s * Cfg::kBBytes, loB_s + sl * Cfg::kBBytes, st);
           ptx::fence_proxy_async_smem();
         }
@@ -574,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<CG>(tmem_base, Cfg::kTmemCols);
+    ptx::tmem_dealloc<CG>(tmem_base, kTmemCols);
   }
 }
 
