@@ -95,11 +95,14 @@ __global__ void __launch_bounds__(STHREADS, 2) k_sgemm_simt(SimtParams p) {
   store_tiles(0);
   __syncthreads();
 
-  float acc[8][8];
+  // Accumulators as column pairs for the packed FP32 FMA (fma.rn.f32x2 =
+  // FFMA2: two independent round-to-nearest FMAs per instruction, so the
+  // results are identical to scalar FFMA with half the issue slots).
+  unsigned long long acc2[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
 
   for (int64_t kb = 0; kb < nk; ++kb) {
     const int cur = static_cast<int>(kb & 1);
@@ -109,14 +112,17 @@ __global__ void __launch_bounds__(STHREADS, 2) k_sgemm_simt(SimtParams p) {
     for (int kk = 0; kk < SBK; ++kk) {
       const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][kk][ty * 4]);
       const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][kk][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[cur][kk][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[cur][kk][64 + tx * 4]);
+      const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][tx * 4]);
+      const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[cur][kk][64 + tx * 4]);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const unsigned long long bp[4] = {b0.x, b0.y, b1.x, b1.y};  // column pairs (j, j+1)
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 8; ++i) {
+        unsigned long long ap;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(ap) : "f"(av[i]));
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[i][j]) : "l"(ap), "l"(bp[j]));
+      }
     }
     if (more) {
       store_tiles(cur ^ 1);
@@ -125,6 +131,11 @@ __global__ void __launch_bounds__(STHREADS, 2) k_sgemm_simt(SimtParams p) {
   }
 
   // ---------------------------------------------------------------- epilogue
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[i][2 * j]), "=f"(acc[i][2 * j + 1]) : "l"(acc2[i][j]));
   const bool full_tile = (row0 + SBM <= p.m) && (col0 + SBN <= p.n);
   const float alpha = p.alpha, beta = p.beta;
 #pragma unroll
