@@ -206,6 +206,13 @@ tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t 
                                   float* B_full, int64_t ldb, float beta, float* C_local,
                                   int64_t ldc, void* stream);
 
+/* Failure detection: polls the communicator for asynchronous NCCL errors
+ * (e.g. a peer died or a network/NVLink fault).  TM_OK if healthy (or an
+ * operation is still in progress), TM_ERR_NCCL if an error was reported; with
+ * abort_on_error != 0 the communicator is then aborted so that blocked
+ * collectives return (tm_comm_destroy must still be called). */
+tm_status tm_comm_check(tm_comm_t comm, int abort_on_error);
+
 /* Bytes this rank received over the communicator since tm_comm_init
  * (message-conservation accounting used by the tests). */
 tm_status tm_comm_bytes_received(tm_comm_t comm, uint64_t* bytes);

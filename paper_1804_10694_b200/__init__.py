@@ -27,7 +27,7 @@ lib_path = os.path.join(_PKG, "_lib", "libtm.so")
 EXPORTED_SYMBOLS = [
     "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_op", "tm_sgemm_colmajor", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
     "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
-    "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_bytes_received",
+    "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
 ]
 
 
@@ -60,6 +60,7 @@ def _load():
     L.tm_comm_init.argtypes = [ctypes.POINTER(vp), ci, ci, vp]
     L.tm_comm_destroy.argtypes = [vp]
     L.tm_comm_rank.argtypes = [vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]
+    L.tm_comm_check.argtypes = [vp, ci]
     L.tm_comm_bytes_received.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
     L.tm_sgemm_dist.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, i64, ci, f32, vp, i64, vp]
     L.tm_sgemm_dist_loopback.argtypes = [ci, ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, vp]
@@ -273,6 +274,10 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+    def check(self, abort_on_error: bool = False) -> bool:
+        """True if no asynchronous NCCL error was reported (failure detection)."""
+        return lib.tm_comm_check(self.handle, int(abort_on_error)) == 0
 
     def bytes_received(self) -> int:
         v = ctypes.c_uint64()

@@ -1,6 +1,7 @@
 // api.cpp -- the C ABI (include/tm.h): argument validation, special cases,
 // path selection and the end-to-end host-buffer entry.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -141,6 +142,12 @@ tm_status run(const GemmArgs& a, int algo, cudaStream_t stream, int sm_reserve =
   // NCCL broadcast must be able to run beside the persistent GEMM).
   const int sms = (sm_reserve > 0 && dev->sms - sm_reserve >= 2) ? dev->sms - sm_reserve : dev->sms;
   Plan pl = make_plan(a, algo, sms);
+  // NVTX range around the enqueue (visible in Nsight Systems; no-op without a tool)
+  struct Range {
+    explicit Range(const char* n) { nvtxRangePushA(n); }
+    ~Range() { nvtxRangePop(); }
+  } range(pl.path == Path::kTc ? (pl.tc.streamk ? "tm_sgemm tf32x3 stream-K" : "tm_sgemm tf32x3")
+                               : pl.path == Path::kSimt ? "tm_sgemm simt" : "tm_sgemm scale");
   if (log_enabled())
     std::fprintf(stderr, "[tm] sgemm m=%lld n=%lld k=%lld algo=%d -> %s cg=%d bn=%d split3=%d\n",
                  static_cast<long long>(a.m), static_cast<long long>(a.n), static_cast<long long>(a.k), algo,

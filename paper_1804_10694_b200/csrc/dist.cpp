@@ -18,6 +18,7 @@
 // with maxCTAs = kCommCtas and the chunk GEMMs leave kCommCtas SMs free.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -63,6 +64,8 @@ struct Nccl {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, NcclConfig*) = nullptr;
   ncclResult_t (*GetVersion)(int*) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
@@ -85,6 +88,9 @@ void load_nccl() {
   g_nccl.CommInitRankConfig =
       reinterpret_cast<decltype(g_nccl.CommInitRankConfig)>(dlsym(h, "ncclCommInitRankConfig"));
   g_nccl.GetVersion = reinterpret_cast<decltype(g_nccl.GetVersion)>(dlsym(h, "ncclGetVersion"));
+  g_nccl.CommGetAsyncError =
+      reinterpret_cast<decltype(g_nccl.CommGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+  g_nccl.CommAbort = reinterpret_cast<decltype(g_nccl.CommAbort)>(dlsym(h, "ncclCommAbort"));
   g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
   g_nccl.Broadcast = reinterpret_cast<decltype(g_nccl.Broadcast)>(dlsym(h, "ncclBroadcast"));
   g_nccl.AllGather = reinterpret_cast<decltype(g_nccl.AllGather)>(dlsym(h, "ncclAllGather"));
@@ -170,7 +176,7 @@ tm_status tm_comm_destroy(tm_comm_t c) {
   if (!c) return TM_ERR_INVALID_VALUE;
   tm_status st = TM_OK;
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->comm && g_nccl.CommDestroy(c->comm) != ncclSuccess) st = TM_ERR_NCCL;
+  if (c->comm && g_nccl.CommDestroy(c->comm) != ncclSuccess) st = TM_ERR_NCCL;  // null after an abort
   for (int i = 0; i < kMaxChunks; ++i)
     if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
@@ -184,6 +190,19 @@ tm_status tm_comm_rank(tm_comm_t c, int* rank, int* nranks) {
   *rank = c->rank;
   *nranks = c->nranks;
   return TM_OK;
+}
+
+tm_status tm_comm_check(tm_comm_t c, int abort_on_error) {
+  if (!c || !c->comm) return TM_ERR_INVALID_VALUE;
+  if (!g_nccl.CommGetAsyncError) return TM_OK;
+  ncclResult_t async = ncclSuccess;
+  if (g_nccl.CommGetAsyncError(c->comm, &async) != ncclSuccess) return TM_ERR_NCCL;
+  if (async == ncclSuccess || static_cast<int>(async) == 7 /* ncclInProgress */) return TM_OK;
+  if (abort_on_error && g_nccl.CommAbort) {
+    g_nccl.CommAbort(c->comm);
+    c->comm = nullptr;
+  }
+  return TM_ERR_NCCL;
 }
 
 tm_status tm_comm_bytes_received(tm_comm_t c, uint64_t* bytes) {
@@ -244,6 +263,10 @@ tm_status dist_schedule(int nranks, int rank, int root, int64_t m, int64_t n, in
   if (nchunks > kMaxChunks) return TM_ERR_INTERNAL;
   if (cudaEventRecord(ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
   if (cudaStreamWaitEvent(comm_stream, ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
+  nvtxRangePushA("tm_sgemm_dist schedule");
+  struct Pop {
+    ~Pop() { nvtxRangePop(); }
+  } pop;
   int used = 0;
   for (int64_t k0 = 0; k0 < k; k0 += kc, ++used) {
     const int64_t kr = (k0 + kc <= k) ? kc : k - k0;
