@@ -54,6 +54,8 @@ def _load():
         lib.tm_oracle_sgemm_op_rows.argtypes = [ctypes.c_int, ctypes.c_int, i64, i64, i64, f32, vp, i64, vp, i64,
                                                 f32, vp, i64, i64, vp, vp, vp, i64]
         lib.tm_oracle_sgemm_op_rows.restype = ctypes.c_int
+        lib.tm_oracle_conv2d_nhwc.argtypes = [i64] * 8 + [f32, vp, vp, f32, vp, i64, vp, vp, vp]
+        lib.tm_oracle_conv2d_nhwc.restype = ctypes.c_int
         lib.tm_oracle_sgemm_f64.argtypes = [i64, i64, i64, f32, vp, i64, vp, i64,
                                             f32, vp, i64, vp, vp, i64]
         lib.tm_oracle_sgemm_f64.restype = ctypes.c_int
@@ -122,6 +124,31 @@ def sgemm(alpha, A, B, beta, C0, rows=None, m=None, n=None, k=None, opa="N", opb
     if rc != 0:
         raise ValueError(f"tm_oracle_sgemm_rows rejected its arguments (rc={rc})")
     return R, D
+
+
+def conv2d_nhwc(alpha, X, Wt, beta, Y0, pad, pixels=None):
+    """R, D (fp64, shape (npix, F)) for the NHWC / KRSC stride-1 convolution
+    Y = alpha * conv(X, Wt) + beta * Y0 (oracle.c: tm_oracle_conv2d_nhwc).
+    X: (Nb, H, W, C) float32, Wt: (F, R, S, C) float32, Y0: (Nb, Ho, Wo, F) or None."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    Wt = np.ascontiguousarray(Wt, dtype=np.float32)
+    Nb, H, W, C = X.shape
+    F, R, S, C2 = Wt.shape
+    assert C == C2
+    Ho, Wo = H + 2 * pad - R + 1, W + 2 * pad - S + 1
+    Y0c = None if Y0 is None else np.ascontiguousarray(Y0, dtype=np.float32)
+    if pixels is None:
+        npix, pix = Nb * Ho * Wo, None
+    else:
+        pix = np.ascontiguousarray(pixels, dtype=np.int64)
+        npix = pix.shape[0]
+    Rr = np.empty((npix, F), np.float64)
+    Dd = np.empty((npix, F), np.float64)
+    rc = _load().tm_oracle_conv2d_nhwc(Nb, H, W, C, F, R, S, pad, float(alpha), _ptr(X), _ptr(Wt), float(beta),
+                                       _ptr(Y0c), npix, _ptr(pix), _ptr(Rr), _ptr(Dd))
+    if rc != 0:
+        raise ValueError(f"tm_oracle_conv2d_nhwc rejected its arguments (rc={rc})")
+    return Rr, Dd
 
 
 def dist_rows(m, nranks, rank):

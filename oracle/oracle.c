@@ -198,3 +198,67 @@ int tm_oracle_get_threads(void) {
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------
+ * Convolution oracle ("sgemm (matrix
+ * multiplication used to implement convolutions)", Conv: 512x512 input, 16
+ * features, batch 32, filters 3x3..11x11).  The plain definition, fp64:
+ *
+ *   Y[b,y,x,f] = alpha * sum_{ky<R, kx<S, c<C} X[b, y+ky-pad, x+kx-pad, c] * Wt[f,ky,kx,c]
+ *                + beta * Y0[b,y,x,f]
+ *   D[b,y,x,f] = |alpha| * sum |X||Wt| + |beta| |Y0|      (acceptance denominator)
+ *
+ * NHWC activations, KRSC filters (F x R x S x C), stride 1, dilation 1, zero
+ * padding `pad` (X outside [0,H) x [0,W) reads as 0); output Ho = H + 2 pad - R
+ * + 1, Wo = W + 2 pad - S + 1.  Sum order: ky, kx, c ascending.  Special
+ * cases as the GEMM oracle (beta == 0 does not read Y0; alpha == 0 does not
+ * read X, Wt).  R, D are (Nb*Ho*Wo) x F row-major (ldr = F); `pixels` selects
+ * output pixels (flattened b*Ho*Wo + y*Wo + x), NULL = all.
+ * ---------------------------------------------------------------------- */
+int tm_oracle_conv2d_nhwc(int64_t Nb, int64_t H, int64_t W, int64_t C, int64_t F, int64_t R, int64_t S,
+                          int64_t pad, float alpha, const float *X, const float *Wt, float beta,
+                          const float *Y0, int64_t npix, const int64_t *pixels, double *Rout, double *Dout) {
+    if (Nb < 0 || H < 1 || W < 1 || C < 1 || F < 1 || R < 1 || S < 1 || pad < 0) return -1;
+    const int64_t Ho = H + 2 * pad - R + 1, Wo = W + 2 * pad - S + 1;
+    if (Ho < 1 || Wo < 1) return -1;
+    const int64_t P = Nb * Ho * Wo;
+    if (!pixels && npix != P) return -1;
+    if (npix < 0 || (npix > 0 && (!Rout || !Dout))) return -1;
+    if (alpha != 0.0f && (!X || !Wt)) return -1;
+    if (beta != 0.0f && !Y0) return -1;
+    if (pixels)
+        for (int64_t t = 0; t < npix; ++t)
+            if (pixels[t] < 0 || pixels[t] >= P) return -1;
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < npix; ++t) {
+        const int64_t q = pixels ? pixels[t] : t;
+        const int64_t b = q / (Ho * Wo), y = (q / Wo) % Ho, x = q % Wo;
+        for (int64_t f = 0; f < F; ++f) {
+            double acc = 0.0, acc_abs = 0.0;
+            if (alpha != 0.0f) {
+                for (int64_t ky = 0; ky < R; ++ky) {
+                    const int64_t iy = y + ky - pad;
+                    for (int64_t kx = 0; kx < S; ++kx) {
+                        const int64_t ix = x + kx - pad;
+                        for (int64_t c = 0; c < C; ++c) {
+                            const double xv = (iy < 0 || iy >= H || ix < 0 || ix >= W)
+                                                  ? 0.0 : (double)X[((b * H + iy) * W + ix) * C + c];
+                            const double wv = (double)Wt[((f * R + ky) * S + kx) * C + c];
+                            acc += xv * wv;
+                            acc_abs += fabs(xv) * fabs(wv);
+                        }
+                    }
+                }
+            }
+            double r = (double)alpha * acc, d = fabs((double)alpha) * acc_abs;
+            if (beta != 0.0f) {
+                const double c0 = (double)Y0[q * F + f];
+                r += (double)beta * c0;
+                d += fabs((double)beta) * fabs(c0);
+            }
+            Rout[t * F + f] = r;
+            Dout[t * F + f] = d;
+        }
+    }
+    return 0;
+}
