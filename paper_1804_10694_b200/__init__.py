@@ -25,7 +25,7 @@ lib_path = os.path.join(_PKG, "_lib", "libtm.so")
 
 # Every function include/tm.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = [
-    "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_op", "tm_sgemm_colmajor", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
+    "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_op", "tm_sgemm_colmajor", "tm_conv2d_nhwc", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
     "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
     "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
 ]
@@ -50,6 +50,7 @@ def _load():
     L.tm_sgemm_host.argtypes = gemm + [ci]
     L.tm_sgemm_op.argtypes = [ci, ci] + gemm + [ci]
     L.tm_sgemm_colmajor.argtypes = [ctypes.c_char, ctypes.c_char] + gemm
+    L.tm_conv2d_nhwc.argtypes = [i64] * 8 + [f32, vp, vp, f32, vp, vp, ci]
     L.tm_sgemm_plan_name.argtypes = [i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, ci]
     L.tm_sgemm_plan_name.restype = ctypes.c_char_p
     L.tm_status_string.argtypes = [ci]
@@ -155,6 +156,23 @@ def sgemm_op(A, B, C, alpha: float = 1.0, beta: float = 0.0, opa: str = "N", opb
                          _ptr(C), _ld(C), _stream(stream), int(algo))
     _check(st, "tm_sgemm_op")
     return C
+
+
+def conv2d_nhwc(X, Wt, Y, alpha: float = 1.0, beta: float = 0.0, pad: int = 0, algo: int = ALGO_AUTO, stream=None):
+    """Y <- alpha * conv(X, Wt) + beta * Y: X (Nb, H, W, C) NHWC, Wt (F, R, S, C)
+    KRSC, Y (Nb, Ho, Wo, F); dense float32 CUDA tensors, stride 1, zero padding."""
+    for name, t in (("X", X), ("Wt", Wt), ("Y", Y)):
+        _f32(name, t)
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    nb, h, w, c = X.shape
+    f, r, s, c2 = Wt.shape
+    if c2 != c or tuple(Y.shape) != (nb, h + 2 * pad - r + 1, w + 2 * pad - s + 1, f):
+        raise ValueError("shape mismatch")
+    st = lib.tm_conv2d_nhwc(nb, h, w, c, f, r, s, pad, float(alpha), _ptr(X), _ptr(Wt), float(beta), _ptr(Y),
+                            _stream(stream), int(algo))
+    _check(st, "tm_conv2d_nhwc")
+    return Y
 
 
 def sgemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None):

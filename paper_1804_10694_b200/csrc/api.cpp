@@ -283,6 +283,55 @@ tm_status tm_sgemm(int64_t m, int64_t n, int64_t k, float alpha, const float* A,
   return tm_sgemm_ex(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, stream, TM_ALGO_AUTO);
 }
 
+// Implicit-GEMM convolution.
+tm_status tm_conv2d_nhwc(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f, int64_t r, int64_t s, int64_t pad,
+                         float alpha, const float* X, const float* Wt, float beta, float* Y, void* stream_, int algo) {
+  try {
+    tmk::ConvArgs a{nb, h, w, c, f, r, s, pad, alpha, beta, X, Wt, Y};
+    if (nb < 0 || h < 1 || w < 1 || c < 1 || f < 1 || r < 1 || s < 1 || pad < 0) return TM_ERR_INVALID_VALUE;
+    if (algo < TM_ALGO_AUTO || algo > TM_ALGO_SIMT_F32) return TM_ERR_INVALID_VALUE;
+    if (a.ho() < 1 || a.wo() < 1) return TM_ERR_INVALID_VALUE;
+    const int64_t P = nb * a.ho() * a.wo();
+    if (P == 0) return TM_OK;
+    if (!Y) return TM_ERR_INVALID_VALUE;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    if (alpha != 0.0f && (!X || !Wt)) return TM_ERR_INVALID_VALUE;
+    // Y must not overlap the inputs it is computed from
+    const int64_t ybytes = P * f * 4;
+    if (alpha != 0.0f && (tmk::ranges_overlap(Y, ybytes, X, nb * h * w * c * 4) ||
+                          tmk::ranges_overlap(Y, ybytes, Wt, f * r * s * c * 4)))
+      return TM_ERR_INVALID_VALUE;
+    tmk::DevInfo* dev = nullptr;
+    tm_status st = tmk::current_device(&dev);
+    if (st != TM_OK) return st;
+    if (alpha == 0.0f) return tmk::launch_scale(P, f, beta, Y, f, stream);
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    const bool tc_ok = (c % 16 == 0) && (f % 4 == 0) && al16(X) && al16(Wt) && al16(Y) && pad <= 127 &&
+                       r <= 128 && s <= 128;
+    if (algo == TM_ALGO_TF32X3 && !tc_ok) return TM_ERR_INVALID_VALUE;
+    if (algo == TM_ALGO_SIMT_F32 || !tc_ok) return tmk::launch_conv_simt(a, stream);
+    const int bk = (c % 32 == 0) ? 32 : 16;
+    int cg = 1, bn = 16;
+    if (f <= 16) { cg = 1; bn = 16; }
+    else if (f <= 32) { cg = 1; bn = 32; }
+    else if (f <= 64) { cg = 1; bn = 64; }
+    else if (bk == 32 && f > 128) { cg = 2; bn = 128; }
+    else { cg = 2; bn = 64; }
+    const char* force = std::getenv("TM_CONV_CONFIG");  // "cg,bn" -- tests only
+    if (force) std::sscanf(force, "%d,%d", &cg, &bn);
+    const int64_t tile_m = 128LL * cg, tile_n = static_cast<int64_t>(bn) * cg;
+    const int64_t tiles = ((P + tile_m - 1) / tile_m) * ((f + tile_n - 1) / tile_n);
+    const bool sk = tiles % (dev->sms / cg) != 0 && tiles < 8LL * (dev->sms / cg);
+    if (tmk::log_enabled())
+      std::fprintf(stderr, "[tm] conv P=%lld F=%lld K=%lld -> tf32x3 cg=%d bn=%d bk=%d streamk=%d\n",
+                   static_cast<long long>(P), static_cast<long long>(f), static_cast<long long>(r * s * c), cg, bn, bk,
+                   sk ? 1 : 0);
+    return tmk::launch_conv_tc(a, cg, bn, bk, sk, dev->sms, stream);
+  } catch (...) {
+    return TM_ERR_INTERNAL;
+  }
+}
+
 tm_status tm_sgemm_op(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda,
                       const float* B, int64_t ldb, float beta, float* C, int64_t ldc, void* stream, int algo) {
   if ((opa != TM_OP_N && opa != TM_OP_T) || (opb != TM_OP_N && opb != TM_OP_T)) return TM_ERR_INVALID_VALUE;

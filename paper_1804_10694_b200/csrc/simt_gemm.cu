@@ -180,7 +180,69 @@ __global__ void k_scale_c(int64_t m, int64_t n, float beta, float* __restrict__ 
   }
 }
 
+// Direct NHWC / KRSC convolution, FP32 FFMA (validation path for the
+// implicit-GEMM tensor-core kernel and fallback for any shape): one thread per
+// output pixel, 16 filters per thread (blockIdx.y selects the filter group);
+// the group's filter taps are staged in shared memory per (ky, kx).
+constexpr int kConvF = 16;
+__global__ void __launch_bounds__(128) k_conv_simt(ConvArgs a) {
+  extern __shared__ float wsh[];  // [kConvF][C] filters of one tap
+  const int64_t ho = a.ho(), wo = a.wo();
+  const int64_t P = a.nb * ho * wo;
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int f0 = blockIdx.y * kConvF;
+  const int nf = static_cast<int>(a.f - f0 < kConvF ? a.f - f0 : kConvF);
+  int64_t b = 0, y = 0, x = 0;
+  if (q < P) {
+    b = q / (ho * wo);
+    y = (q / wo) % ho;
+    x = q % wo;
+  }
+  float acc[kConvF];
+#pragma unroll
+  for (int j = 0; j < kConvF; ++j) acc[j] = 0.0f;
+  for (int64_t ky = 0; ky < a.r; ++ky) {
+    for (int64_t kx = 0; kx < a.s; ++kx) {
+      __syncthreads();
+      for (int64_t i = threadIdx.x; i < static_cast<int64_t>(nf) * a.c; i += blockDim.x) {
+        const int64_t fj = i / a.c, c = i - fj * a.c;
+        wsh[fj * a.c + c] = a.Wt[(((f0 + fj) * a.r + ky) * a.s + kx) * a.c + c];
+      }
+      __syncthreads();
+      const int64_t iy = y + ky - a.pad, ix = x + kx - a.pad;
+      if (q < P && iy >= 0 && iy < a.h && ix >= 0 && ix < a.w) {
+        const float* xp = a.X + ((b * a.h + iy) * a.w + ix) * a.c;
+        for (int64_t c = 0; c < a.c; ++c) {
+          const float xv = __ldg(xp + c);
+#pragma unroll
+          for (int j = 0; j < kConvF; ++j)
+            if (j < nf) acc[j] = fmaf(xv, wsh[j * a.c + c], acc[j]);
+        }
+      }
+    }
+  }
+  if (q < P) {
+    float* yp = a.Y + q * a.f + f0;
+#pragma unroll
+    for (int j = 0; j < kConvF; ++j)
+      if (j < nf) yp[j] = (a.beta == 0.0f) ? a.alpha * acc[j] : fmaf(a.alpha, acc[j], a.beta * yp[j]);
+  }
+}
+
 }  // namespace
+
+tm_status launch_conv_simt(const ConvArgs& a, cudaStream_t stream) {
+  const int64_t P = a.nb * a.ho() * a.wo();
+  const int64_t blocks = (P + 127) / 128;
+  const int64_t fgroups = (a.f + kConvF - 1) / kConvF;
+  const size_t smem = static_cast<size_t>(kConvF) * a.c * 4;
+  if (blocks > INT32_MAX || fgroups > 65535 || smem > 160 * 1024) return TM_ERR_INVALID_VALUE;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(k_conv_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+    return TM_ERR_CUDA;
+  k_conv_simt<<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(fgroups)), 128, smem, stream>>>(a);
+  return cudaGetLastError() == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+}
 
 tm_status launch_simt(const GemmArgs& a, cudaStream_t stream) {
   SimtParams p;

@@ -59,32 +59,27 @@ constexpr int kEpiStride = 20;     // floats per staged row (16 data + 4 pad: 16
 constexpr int kKcBlocksDefault = 4;   // K_c = 4 * 32 = 128: RZ partial length before RN promotion
 constexpr int kGroupMDefault = 16;    // raster: tile-rows per group (L2 reuse)
 
-template <int BN_CTA>
-struct StageCfg;
-template <>
-struct StageCfg<128> { static constexpr int kRaw = 4, kLo = 2; };
-template <>
-struct StageCfg<64> { static constexpr int kRaw = 6, kLo = 2; };
-template <>
-struct StageCfg<32> { static constexpr int kRaw = 8, kLo = 2; };
-
-template <int CG, int BN_CTA, bool SPLIT3>
+// Stage ring sizes from a shared-memory budget: two lo stages, as many raw
+// (TMA) stages as fit, at most 12.
+template <int CG, int BN_CTA, bool SPLIT3, int BK = 32>
 struct TcCfg {
-  static constexpr int kRaw = StageCfg<BN_CTA>::kRaw;
-  static constexpr int kLo = StageCfg<BN_CTA>::kLo;  // ready/empty_lo ring depth (no lo smem if !SPLIT3)
-  static constexpr int kABytes = kBMCta * kBK * 4;   // 16 KiB
-  static constexpr int kBBytes = kBK * BN_CTA * 4;   // BN_CTA/32 boxes of 4 KiB
+  static constexpr int kABytes = kBMCta * BK * 4;    // 16 KiB (BK 32) / 8 KiB (BK 16)
+  static constexpr int kBBytes = BK * BN_CTA * 4;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kLo = 2;                      // ready/empty_lo ring depth (no lo smem if !SPLIT3)
+  static constexpr int kRawFit = (200 * 1024 - kLo * kStage) / kStage;
+  static constexpr int kRaw = kRawFit < 12 ? kRawFit : 12;
   static constexpr int kMmaM = kBMCta * CG;
   static constexpr int kMmaN = BN_CTA * CG;
   static constexpr int kTileM = kMmaM;
   static constexpr int kTileN = kMmaN;
   static constexpr int kCols = kMmaN / 2;            // columns per promotion warp
-  static constexpr int kTmemCols = (2 * kMmaN <= 32) ? 32 : (2 * kMmaN <= 64) ? 64 : (2 * kMmaN <= 128) ? 128 : (2 * kMmaN <= 256) ? 256 : 512;
-  static constexpr int kRawBytes = kRaw * (kABytes + kBBytes);
-  static constexpr int kLoBytes = SPLIT3 ? kLo * (kABytes + kBBytes) : 0;
+  static constexpr int kRawBytes = kRaw * kStage;
+  static constexpr int kLoBytes = SPLIT3 ? kLo * kStage : 0;
   static constexpr int kNumBars = 2 * kRaw + 2 * kLo + 4;
   static constexpr int kEpiStageBytes = kEpiWarps * 32 * kEpiStride * 4;  // transpose staging
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kRawBytes + kLoBytes + kEpiStageBytes + kNumBars * 8 + 16;
+  static_assert(kRaw >= 3, "ring too shallow");
 };
 
 struct TcParams {
@@ -108,6 +103,9 @@ struct TcParams {
   unsigned long long* trace;  // debug timeline [grid][kTraceSlots] (%globaltimer ns) or null
   unsigned* wave_ctr;         // data-parallel wave barrier counter (zeroed per launch) or null
   int full_waves;             // waves in which every cluster has a tile
+  // implicit-GEMM convolution (CONV kernels): GEMM row = output pixel
+  // (b, y, x) of an Nb x Ho x Wo grid, K index = (ky*S + kx)*C + c.
+  int cv_ho, cv_wo, cv_s, cv_c, cv_pad;
 };
 
 constexpr int kTraceSlots = 8;
@@ -139,15 +137,23 @@ __device__ __forceinline__ uint4 tf32_lo4(uint4 v) {
 // layout) with 128 threads, 8 loads in flight per thread.
 template <int BYTES>
 __device__ __forceinline__ void split_tile(uint32_t src, uint32_t dst, int st) {
-  constexpr int kIters = BYTES / 16 / kSplitThreads;
+  constexpr int kChunks = BYTES / 16;
+  constexpr int kIters = (kChunks + kSplitThreads - 1) / kSplitThreads;
   constexpr int kBatch = kIters < 8 ? kIters : 8;
+  constexpr bool kRagged = kChunks % kSplitThreads != 0;  // tiles smaller than 128 x 16 B
 #pragma unroll
   for (int b = 0; b < kIters; b += kBatch) {
     uint4 v[kBatch];
 #pragma unroll
-    for (int i = 0; i < kBatch; ++i) v[i] = ptx::lds128(src + ((b + i) * kSplitThreads + st) * 16);
+    for (int i = 0; i < kBatch; ++i) {
+      const int idx = (b + i) * kSplitThreads + st;
+      if (!kRagged || idx < kChunks) v[i] = ptx::lds128(src + idx * 16);
+    }
 #pragma unroll
-    for (int i = 0; i < kBatch; ++i) ptx::sts128(dst + ((b + i) * kSplitThreads + st) * 16, tf32_lo4(v[i]));
+    for (int i = 0; i < kBatch; ++i) {
+      const int idx = (b + i) * kSplitThreads + st;
+      if (!kRagged || idx < kChunks) ptx::sts128(dst + idx * 16, tf32_lo4(v[i]));
+    }
   }
 }
 
@@ -221,22 +227,26 @@ template <int KCOLS>
 __device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, int m, int n, int row0, int col0,
                                           const float (&acc)[KCOLS], float alpha, float beta, float* stage,
                                           int lane) {
+  constexpr int SWD = KCOLS < 16 ? KCOLS : 16;  // slab width (columns)
+  constexpr int G = SWD / 4;                     // 16-byte groups per slab row
+  constexpr int RPI = 32 / G;                    // rows covered by one warp-wide access
+  constexpr int NI = 32 / RPI;                   // accesses per slab
 #pragma unroll
-  for (int c = 0; c < KCOLS; c += 16) {
+  for (int c = 0; c < KCOLS; c += SWD) {
 #pragma unroll
-    for (int j = 0; j < 16; j += 4)
+    for (int j = 0; j < SWD; j += 4)
       *reinterpret_cast<float4*>(stage + lane * kEpiStride + j) =
           make_float4(acc[c + j], acc[c + j + 1], acc[c + j + 2], acc[c + j + 3]);
     __syncwarp();
-    const int cc = (lane & 3) * 4;
+    const int cc = (lane % G) * 4;
     const int col = col0 + c + cc;
     const bool full_cols = col + 3 < n;
 #pragma unroll
-    for (int i0 = 0; i0 < 4; i0 += 2) {  // two 8-row groups per round: 2 C loads in flight, low register use
+    for (int i0 = 0; i0 < NI; i0 += 2) {  // two row groups per round: 2 C loads in flight, low register use
       float4 v[2], cv[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int r = (i0 + i) * 8 + (lane >> 2);
+        const int r = (i0 + i) * RPI + lane / G;
         v[i] = *reinterpret_cast<const float4*>(stage + r * kEpiStride + cc);
         cv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         const int row = row0 + r;
@@ -253,7 +263,7 @@ __device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, 
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int row = row0 + (i0 + i) * 8 + (lane >> 2);
+        const int row = row0 + (i0 + i) * RPI + lane / G;
         if (row >= m) continue;
         float4 o;
         if (beta == 0.0f) {
@@ -278,18 +288,26 @@ __device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, 
 
 // TA / TB: op(A) = A^T (A stored k x m, M contiguous -> MN-major A operand) /
 // op(B) = B^T (B stored n x k, K contiguous -> K-major B operand).
-template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB>
+// BK: K elements per stage, 32 (128-B K-major rows, SWIZZLE_128B) or 16 (64-B
+// rows, SWIZZLE_64B; K-major operands only).
+// CONV: A is the implicit im2col matrix of an NHWC activation tensor, loaded
+// with TMA im2col-mode copies (one filter tap x BK channels per stage).
+template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB, int BK = 32, bool CONV = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
-  using Cfg = TcCfg<CG, BN_CTA, SPLIT3>;
+  using Cfg = TcCfg<CG, BN_CTA, SPLIT3, BK>;
+  static_assert(BK == 32 || BK == 16, "BK");
+  static_assert(BK == 32 || (!TA && TB), "64-B rows only for K-major operands");
+  static_assert(TB || BN_CTA % 32 == 0, "MN-major B needs 32-column atoms");
+  static_assert(!CONV || (!TA && TB), "conv: A = im2col (K-major), B = KRSC filters (K-major)");
   constexpr int RAW = Cfg::kRaw, LO = Cfg::kLo, KCOLS = Cfg::kCols;
   // A_lo staged in TMEM (written by the split warps with tcgen05.st, read by
   // the A_lo*B_hi MMA directly from tensor memory): saves its shared-memory
   // write and read.  Needs K-major A and free TMEM columns beyond the two
   // partial accumulators (not the 2-CTA 256-column tile, whose partials use
   // all 512 columns).
-  constexpr bool ALO = SPLIT3 && !TA && (2 * Cfg::kMmaN + LO * kBK <= 512);
-  constexpr int kTmemNeed = 2 * Cfg::kMmaN + (ALO ? LO * kBK : 0);
+  constexpr bool ALO = SPLIT3 && !TA && (2 * Cfg::kMmaN + LO * BK <= 512);
+  constexpr int kTmemNeed = 2 * Cfg::kMmaN + (ALO ? LO * BK : 0);
   constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
   constexpr uint32_t kAloCol = 2 * Cfg::kMmaN;  // first TMEM column of the A_lo stages
 
@@ -380,19 +398,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::mbar_wait(&empty_raw[s], ph ^ 1);
             ptx::mbar_arrive_expect_tx(&full[s], Cfg::kABytes + Cfg::kBBytes);
-            if constexpr (!TA) {  // A: one K-major box 32 (k) x 128 (rows)
-              ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * kBK, row0);
+            if constexpr (CONV) {
+              // K-block kb = (filter tap, BK-channel chunk).  Output pixel row0
+              // = (b, y, x); its input window starts at (y - pad, x - pad) and
+              // the tap adds (ky, kx) as im2col offsets.  TMA walks 128 output
+              // pixels in W, H, N order and zero-fills outside the image.
+              const int chunks = p.cv_c / BK;
+              const int tap = kb / chunks, c0 = (kb - tap * chunks) * BK;
+              const int ky = tap / p.cv_s, kx = tap - ky * p.cv_s;
+              const int hw = p.cv_ho * p.cv_wo;
+              const int b = row0 / hw, yx = row0 - b * hw;
+              const int y = yx / p.cv_wo, x = yx - y * p.cv_wo;
+              ptx::tma_load_im2col_4d(rawA + s * Cfg::kABytes, &tmA, &full[s], c0, x - p.cv_pad, y - p.cv_pad, b,
+                                      static_cast<uint16_t>(kx), static_cast<uint16_t>(ky));
+            } else if constexpr (!TA) {  // A: one K-major box BK (k) x 128 (rows)
+              ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * BK, row0);
             } else {              // A^T: four MN-major boxes 32 (rows) x 32 (k)
 #pragma unroll
               for (int j = 0; j < kBMCta / 32; ++j)
-                ptx::tma_load_2d(rawA + s * Cfg::kABytes + j * 4096, &tmA, &full[s], row0 + 32 * j, kb * kBK);
+                ptx::tma_load_2d(rawA + s * Cfg::kABytes + j * 4096, &tmA, &full[s], row0 + 32 * j, kb * BK);
             }
             if constexpr (!TB) {  // B: BN_CTA/32 MN-major boxes 32 (cols) x 32 (k)
 #pragma unroll
               for (int j = 0; j < BN_CTA / 32; ++j)
-                ptx::tma_load_2d(rawB + s * Cfg::kBBytes + j * 4096, &tmB, &full[s], col0 + 32 * j, kb * kBK);
-            } else {              // B^T: one K-major box 32 (k) x BN_CTA (cols)
-              ptx::tma_load_2d(rawB + s * Cfg::kBBytes, &tmB, &full[s], kb * kBK, col0);
+                ptx::tma_load_2d(rawB + s * Cfg::kBBytes + j * 4096, &tmB, &full[s], col0 + 32 * j, kb * BK);
+            } else {              // B^T: one K-major box BK (k) x BN_CTA (cols)
+              ptx::tma_load_2d(rawB + s * Cfg::kBBytes, &tmB, &full[s], kb * BK, col0);
             }
             if (++s == RAW) { s = 0; ph ^= 1; }
           }
@@ -407,7 +438,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // K-major tile (rows of 128 B = 32 k, SWIZZLE_128B): K step of 8 = 32 B inside the row.
         // MN-major tile (rows of 128 B = 32 m/n, 32-B-atom swizzle): K step of 8 rows = 1024 B
         // (two 512-B atoms, SBO); 32-column atoms 4096 B apart (LBO).
-        auto desc_k = [](uint32_t base, int ks) { return ptx::sdesc(base + ks * 32, 16, 1024, ptx::kLayoutSW128); };
+        // BK 16: rows of 64 B (16 k), SWIZZLE_64B, 8-row groups 512 B apart.
+        auto desc_k = [](uint32_t base, int ks) {
+          return ptx::sdesc(base + ks * 32, 16, 8 * BK * 4, BK == 32 ? ptx::kLayoutSW128 : ptx::kLayoutSW64);
+        };
         auto desc_mn = [](uint32_t base, int ks) {
           return ptx::sdesc(base + ks * 1024, 4096, 512, ptx::kLayoutSW128Base32B);
         };
@@ -428,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::tc_fence_after();
               if (kb == 0 && s == 0 && ph == 0) trace_mark(p, 4);  // first MMA issue
 #pragma unroll
-              for (int ks = 0; ks < kBK / 8; ++ks) {
+              for (int ks = 0; ks < BK / 8; ++ks) {
                 const uint64_t aH = TA ? desc_mn(rawA_s + s * Cfg::kABytes, ks) : desc_k(rawA_s + s * Cfg::kABytes, ks);
                 const uint64_t bH = TB ? desc_k(rawB_s + s * Cfg::kBBytes, ks) : desc_mn(rawB_s + s * Cfg::kBBytes, ks);
                 const uint32_t acc = (kb != kb0 || ks != 0) ? 1u : 0u;  // fresh partial per K_c chunk
@@ -439,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   // A_hi feeds two MMAs back to back: fetched from smem once (collector fill/lastuse)
                   if constexpr (ALO) {
                     constexpr uint32_t idesc_k = ptx::idesc_tf32(Cfg::kMmaM, Cfg::kMmaN, 0, TB ? 0 : 1);
-                    ptx::mma_tf32_tmem_a<CG>(d, tmem_base + kAloCol + sl * kBK + ks * 8, bH, idesc_k, acc);
+                    ptx::mma_tf32_tmem_a<CG>(d, tmem_base + kAloCol + sl * BK + ks * 8, bH, idesc_k, acc);
                   } else {
                     ptx::mma_tf32<CG>(d, aL, bH, idesc, acc);
                   }
@@ -480,20 +514,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (SPLIT3) {
           if constexpr (ALO) {
             // Row r = this thread's TMEM lane (warp w owns lanes 32*(w%4)..+31):
-            // read its 128-B row of the raw K-major A tile (16-B chunk c lives
-            // at chunk c ^ (r % 8)), split, store 32 columns of A_lo.
+            // read its row of the raw K-major A tile (16-B chunk c of a 128-B
+            // row lives at chunk c ^ (r % 8); of a 64-B row at c ^ ((r/2) % 4)),
+            // split, store BK columns of A_lo.
             const int r = st;
-            const uint32_t rowp = rawA_s + s * Cfg::kABytes + r * 128;
-            uint32_t lo[32];
+            const uint32_t rowp = rawA_s + s * Cfg::kABytes + r * (BK * 4);
+            uint32_t lo[BK];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const uint4 v = ptx::lds128(rowp + ((c ^ (r & 7)) << 4));
+            for (int c = 0; c < BK / 4; ++c) {
+              const int pc = BK == 32 ? (c ^ (r & 7)) : (c ^ ((r >> 1) & 3));
+              const uint4 v = ptx::lds128(rowp + (pc << 4));
               lo[4 * c] = tf32_lo_bits(v.x);
               lo[4 * c + 1] = tf32_lo_bits(v.y);
               lo[4 * c + 2] = tf32_lo_bits(v.z);
               lo[4 * c + 3] = tf32_lo_bits(v.w);
             }
-            ptx::tmem_st_32x32b_x32(tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + kAloCol + sl * kBK, lo);
+            const uint32_t ta = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + kAloCol + sl * BK;
+            if constexpr (BK == 32) ptx::tmem_st_32x32b_x32(ta, lo);
+            else ptx::tmem_st_32x32b_x16(ta, lo);
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
           } else {
@@ -532,13 +570,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                static_cast<uint32_t>(pb * Cfg::kMmaN + h * KCOLS);
+        if constexpr (KCOLS >= 16) {
 #pragma unroll
-        for (int c = 0; c < KCOLS; c += 16) {
-          uint32_t r[16];
-          ptx::tmem_ld_32x32b_x16(taddr + c, r);
+          for (int c = 0; c < KCOLS; c += 16) {
+            uint32_t r[16];
+            ptx::tmem_ld_32x32b_x16(taddr + c, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(r[j]);  // RN promotion
+          }
+        } else {
+          uint32_t r[8];
+          ptx::tmem_ld_32x32b_x8(taddr, r);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[c + j] += __uint_as_float(r[j]);  // RN promotion
+          for (int j = 0; j < 8; ++j) acc[j] += __uint_as_float(r[j]);  // RN promotion
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -650,45 +696,25 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, 
   return r == CUDA_SUCCESS;
 }
 
-template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB>
-tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t stream) {
-  using Cfg = TcCfg<CG, BN_CTA, SPLIT3>;
-  auto kern = k_sgemm_tc<CG, BN_CTA, SPLIT3, TA, TB>;
+// Common launch: p carries the problem (m, n, k, tiles, kblocks, C, alpha,
+// beta, and the conv geometry for CONV kernels); this fills the schedule
+// (stream-K / wave barrier / tuning knobs) and launches the cluster kernel.
+template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB, int BK, bool CONV>
+tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams p, int num_sms, bool streamk,
+                        cudaStream_t stream) {
+  using Cfg = TcCfg<CG, BN_CTA, SPLIT3, BK>;
+  auto kern = k_sgemm_tc<CG, BN_CTA, SPLIT3, TA, TB, BK, CONV>;
   static bool attr_set = false;  // per instantiation; attribute is per-function, process-wide
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes) != cudaSuccess)
       return TM_ERR_CUDA;
     attr_set = true;
   }
-  CUtensorMap tmA, tmB;
-  // K-major operands (A, B^T): box 32 (k) x rows, SWIZZLE_128B.  MN-major
-  // operands (A^T, B): box 32 (m or n) x 32 (k), 128-B swizzle with 32-B atoms.
-  bool ok;
-  if constexpr (!TA) ok = encode_2d(&tmA, a.A, a.m, a.k, a.lda, kBK, kBMCta, CU_TENSOR_MAP_SWIZZLE_128B);
-  else ok = encode_2d(&tmA, a.A, a.k, a.m, a.lda, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  if (!ok) return TM_ERR_INTERNAL;
-  if constexpr (!TB) ok = encode_2d(&tmB, a.B, a.k, a.n, a.ldb, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  else ok = encode_2d(&tmB, a.B, a.n, a.k, a.ldb, kBK, BN_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!ok) return TM_ERR_INTERNAL;
-  TcParams p;
-  p.A = a.A;
-  p.lda = a.lda;
-  p.m = static_cast<int>(a.m);
-  p.n = static_cast<int>(a.n);
-  p.k = static_cast<int>(a.k);
-  p.tiles_m = static_cast<int>((a.m + Cfg::kTileM - 1) / Cfg::kTileM);
-  p.tiles_n = static_cast<int>((a.n + Cfg::kTileN - 1) / Cfg::kTileN);
-  p.num_tiles = p.tiles_m * p.tiles_n;
-  p.kblocks = static_cast<int>((a.k + kBK - 1) / kBK);
   // Tuning knobs (bench/tests only), read once per process.
   static const int env_kc = [] { const char* e = std::getenv("TM_KC_BLOCKS"); return e ? std::max(1, std::atoi(e)) : 0; }();
   static const int env_gm = [] { const char* e = std::getenv("TM_GROUP_M"); return e ? std::max(1, std::atoi(e)) : 0; }();
-  p.kc_blocks = env_kc ? env_kc : kKcBlocksDefault;
+  p.kc_blocks = env_kc ? env_kc : kKcBlocksDefault * 32 / BK;  // K_c = 128 elements
   p.group_m = env_gm ? env_gm : kGroupMDefault;
-  p.alpha = a.alpha;
-  p.beta = a.beta;
-  p.C = a.C;
-  p.ldc = a.ldc;
   const int max_clusters = num_sms / CG;
   int clusters = p.num_tiles < max_clusters ? p.num_tiles : max_clusters;
   p.iters = static_cast<long long>(p.num_tiles) * p.kblocks;
@@ -764,6 +790,36 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t 
     delete[] h;
   }
   return TM_OK;
+}
+
+template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB>
+tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t stream) {
+  using Cfg = TcCfg<CG, BN_CTA, SPLIT3>;
+  CUtensorMap tmA, tmB;
+  // K-major operands (A, B^T): box 32 (k) x rows, SWIZZLE_128B.  MN-major
+  // operands (A^T, B): box 32 (m or n) x 32 (k), 128-B swizzle with 32-B atoms.
+  bool ok;
+  if constexpr (!TA) ok = encode_2d(&tmA, a.A, a.m, a.k, a.lda, kBK, kBMCta, CU_TENSOR_MAP_SWIZZLE_128B);
+  else ok = encode_2d(&tmA, a.A, a.k, a.m, a.lda, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (!ok) return TM_ERR_INTERNAL;
+  if constexpr (!TB) ok = encode_2d(&tmB, a.B, a.k, a.n, a.ldb, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  else ok = encode_2d(&tmB, a.B, a.n, a.k, a.ldb, kBK, BN_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!ok) return TM_ERR_INTERNAL;
+  TcParams p{};
+  p.A = a.A;
+  p.lda = a.lda;
+  p.m = static_cast<int>(a.m);
+  p.n = static_cast<int>(a.n);
+  p.k = static_cast<int>(a.k);
+  p.tiles_m = static_cast<int>((a.m + Cfg::kTileM - 1) / Cfg::kTileM);
+  p.tiles_n = static_cast<int>((a.n + Cfg::kTileN - 1) / Cfg::kTileN);
+  p.num_tiles = p.tiles_m * p.tiles_n;
+  p.kblocks = static_cast<int>((a.k + kBK - 1) / kBK);
+  p.alpha = a.alpha;
+  p.beta = a.beta;
+  p.C = a.C;
+  p.ldc = a.ldc;
+  return launch_kernel<CG, BN_CTA, SPLIT3, TA, TB, 32, false>(tmA, tmB, p, num_sms, streamk, stream);
 }
 
 template <bool SPLIT3, bool TA, bool TB>

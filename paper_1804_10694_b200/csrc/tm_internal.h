@@ -52,6 +52,27 @@ tm_status sgemm_reserve(const GemmArgs& a, cudaStream_t stream, int sm_reserve);
 tm_status streamk_workspace(cudaStream_t stream, size_t ws_bytes, size_t flag_count, float** ws, unsigned** flags,
                             unsigned* epoch);
 
+// Implicit-GEMM convolution, NHWC activations, KRSC filters, stride 1:
+// Y[b,y,x,f] = alpha * sum X[b, y+ky-pad, x+kx-pad, c] * Wt[f,ky,kx,c] + beta * Y.
+struct ConvArgs {
+  int64_t nb, h, w, c, f, r, s, pad;
+  float alpha, beta;
+  const float* X;
+  const float* Wt;
+  float* Y;
+#ifdef __CUDACC__
+  __host__ __device__
+#endif
+  int64_t ho() const { return h + 2 * pad - r + 1; }
+#ifdef __CUDACC__
+  __host__ __device__
+#endif
+  int64_t wo() const { return w + 2 * pad - s + 1; }
+};
+// bk: channels per stage (16 or 32); cg/bn as TcChoice.
+tm_status launch_conv_tc(const ConvArgs& a, int cg, int bn, int bk, bool streamk, int num_sms, cudaStream_t stream);
+tm_status launch_conv_simt(const ConvArgs& a, cudaStream_t stream);
+
 // Picks the tensor-core configuration for a shape (planner, plan.cpp).
 TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms);
 // Whether a configuration should run stream-K for this shape.

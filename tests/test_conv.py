@@ -1,0 +1,79 @@
+"""Implicit-GEMM convolution (tm_conv2d_nhwc, the
+paper's Conv benchmark PAPER.md:824-826) against the convolution oracle
+(pinned in test_conv_oracle.py): tensor-core path (TMA im2col), every compiled
+configuration, and the SIMT direct-convolution path."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import seeded_inputs as si
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+TF32X3, SIMT, AUTO = 1, 2, 0
+
+
+def _run(shape, algo=AUTO, beta=0.5, config=None, seed=0, kind="uniform"):
+    import torch
+    import paper_1804_10694_b200 as tm
+    Nb, H, W, C, F, R, S, pad = shape
+    g = si.rng(seed + sum(shape))
+    draw = (lambda sh: si.integers(g, sh)) if kind == "integer" else (lambda sh: si.uniform(g, sh))
+    X = draw((Nb, H, W, C))
+    Wt = draw((F, R, S, C))
+    Ho, Wo = H + 2 * pad - R + 1, W + 2 * pad - S + 1
+    Y0 = draw((Nb, Ho, Wo, F))
+    dX, dW, dY = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (X, Wt, Y0))
+    if config:
+        os.environ["TM_CONV_CONFIG"] = config
+    try:
+        tm.conv2d_nhwc(dX, dW, dY, 1.5, beta, pad, algo=algo)
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("TM_CONV_CONFIG", None)
+    return X, Wt, Y0, dY.cpu().numpy().reshape(-1, F)
+
+
+SHAPES = [(2, 9, 11, 16, 16, 3, 3, 1), (1, 7, 6, 16, 16, 3, 3, 0), (2, 13, 10, 32, 64, 3, 5, 2),
+          (1, 8, 8, 16, 32, 7, 7, 3), (3, 20, 17, 64, 48, 1, 1, 0), (1, 33, 35, 16, 8, 5, 3, 1)]
+
+
+@pytest.mark.parametrize("algo", [AUTO, SIMT])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_conv_parity(algo, shape):
+    X, Wt, Y0, Y = _run(shape, algo)
+    R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, shape[-1])
+    assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL
+
+
+@pytest.mark.parametrize("config,shape", [("1,16", (2, 15, 12, 16, 16, 3, 3, 1)), ("1,32", (2, 15, 12, 16, 24, 3, 3, 1)),
+                                          ("1,64", (1, 19, 21, 16, 64, 3, 3, 1)), ("2,64", (2, 19, 21, 16, 96, 3, 3, 1)),
+                                          ("1,16", (2, 15, 12, 32, 16, 3, 3, 1)), ("1,64", (1, 19, 21, 64, 40, 3, 3, 1)),
+                                          ("2,64", (2, 19, 21, 32, 128, 3, 3, 0)), ("2,128", (1, 19, 21, 32, 200, 3, 3, 1))])
+def test_conv_tensor_core_configs(config, shape):
+    X, Wt, Y0, Y = _run(shape, TF32X3, config=config)
+    R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, shape[-1])
+    assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL
+
+
+def test_conv_beta_zero_and_integer_bit_exact():
+    shape = (2, 12, 12, 16, 16, 3, 3, 1)
+    X, Wt, Y0, Y = _run(shape, TF32X3, beta=0.0)
+    R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.0, None, 1)
+    assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL
+    X, Wt, Y0, Y = _run(shape, TF32X3, kind="integer")
+    R, _ = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, 1)
+    assert np.array_equal(Y.astype(np.float64), R)
+
+
+def test_conv_paper_shape_sampled_pixels():
+    """512x512 input, 16 input/output features, batch 32, 3x3."""
+    shape = (32, 512, 512, 16, 16, 3, 3, 1)
+    X, Wt, Y0, Y = _run(shape, AUTO, seed=1808)
+    P = Y.shape[0]
+    g = si.rng(5)
+    pix = np.unique(np.concatenate([g.integers(0, P, 3000), [0, 511, 512, 512 * 511, P - 1, P - 512]]))
+    R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, 1, pixels=pix)
+    assert float(np.max(oracle.normalized_error(Y[pix], R, D))) <= TOL
