@@ -217,13 +217,16 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C3b", "C4", "C5"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C3b", "C4", "C5", "CONV"])
     ap.add_argument("--algo", default="auto", choices=list(ALGOS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--conv-beta", type=float, default=0.0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "CONV":
+        return run_conv(args)
 
     import torch
     import torch.distributed as dist
@@ -350,6 +353,50 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def run_conv(args):
+    """The paper's Conv benchmark shape (512x512 input, 16 input/output
+    features, batch 32, 3x3 filter, here with 'same' padding; a convolution
+    layer, so Y = conv(X, W): alpha 1, beta 0 unless --conv-beta) through the
+    implicit-GEMM tensor-core convolution (not a
+    BASELINE.json config).  Roofline: HBM (X read once, Y written [and read])."""
+    import torch
+    import paper_1804_10694_b200 as tm
+    Nb, H, W, C, F, R, S, pad = 32, 512, 512, 16, 16, 3, 3, 1
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1804)
+    X = torch.rand((Nb, H, W, C), generator=g, device="cuda") * 2 - 1
+    Wt = torch.rand((F, R, S, C), generator=g, device="cuda") * 2 - 1
+    Y = torch.rand((Nb, H, W, F), generator=g, device="cuda") * 2 - 1
+    algo = ALGOS[args.algo]
+    alpha, beta = (1.0, 0.0) if args.conv_beta == 0.0 else (1.5, args.conv_beta)
+    for _ in range(args.warmup):
+        tm.conv2d_nhwc(X, Wt, Y, alpha, beta, pad, algo=algo)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(0) as clocks:
+        for i in range(args.steps):
+            ev[i][0].record()
+            tm.conv2d_nhwc(X, Wt, Y, alpha, beta, pad, algo=algo)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    flops = 2.0 * Nb * H * W * F * R * S * C
+    algo_bytes = 4 * (X.numel() + Wt.numel() + (2 if beta != 0.0 else 1) * Y.numel())
+    peaks = load_peaks()
+    gbs = algo_bytes / (ms * 1e-3) / 1e9
+    line = {"metric": "conv2d (implicit GEMM) GB/s and GFLOP/s", "value": round(gbs, 2), "unit": "GB/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "dtype": "f32 (3xTF32 tensor-core)" if algo != 2 else "f32",
+            "gflops": round(flops / (ms * 1e-3) / 1e9, 1), "data": "synthetic (device-generated U[-1,1))",
+            "config": {"workload": f"PAPER.md:826 Conv: NHWC 32x512x512x16, KRSC 16x3x3x16, pad 1, alpha {alpha} beta {beta}",
+                       "l2": "inputs larger than L2, no flush"},
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": None},
+            "clocks": clocks.summary()}
+    print(json.dumps(line), flush=True)
     return 0
 
 

@@ -55,27 +55,37 @@ constexpr int kBMCta = 128;        // A rows per CTA
 constexpr int kThreads = 512;
 constexpr int kSplitThreads = 128;
 constexpr int kEpiWarps = 8;
+constexpr int kProducers = 3;      // TMA-issuing warps (0, 2, 3)
 constexpr int kEpiStride = 20;     // floats per staged row (16 data + 4 pad: 16-B aligned, few bank conflicts)
 constexpr int kKcBlocksDefault = 4;   // K_c = 4 * 32 = 128: RZ partial length before RN promotion
 constexpr int kGroupMDefault = 16;    // raster: tile-rows per group (L2 reuse)
 
-// Stage ring sizes from a shared-memory budget: two lo stages, as many raw
-// (TMA) stages as fit, at most 12.
-template <int CG, int BN_CTA, bool SPLIT3, int BK = 32>
+// Stage ring sizes from a shared-memory budget.  With A_lo in TMEM (kAlo: K-major
+// A and room for at least two A_lo stages beyond the two partial accumulators)
+// the lo ring holds only B_lo in shared memory and A_lo in TMEM columns, so it
+// is made as deep as TMEM allows (<= 8; also 8 for 1xTF32): for skinny tiles a stage carries only
+// a few short MMAs, and a 2-deep split -> MMA -> commit round trip would bound
+// the rate.  Otherwise two lo stages; as many raw (TMA) stages as fit, <= 12.
+template <int CG, int BN_CTA, bool SPLIT3, int BK = 32, bool TA = false>
 struct TcCfg {
   static constexpr int kABytes = kBMCta * BK * 4;    // 16 KiB (BK 32) / 8 KiB (BK 16)
   static constexpr int kBBytes = BK * BN_CTA * 4;
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kLo = 2;                      // ready/empty_lo ring depth (no lo smem if !SPLIT3)
-  static constexpr int kRawFit = (200 * 1024 - kLo * kStage) / kStage;
-  static constexpr int kRaw = kRawFit < 12 ? kRawFit : 12;
   static constexpr int kMmaM = kBMCta * CG;
   static constexpr int kMmaN = BN_CTA * CG;
+  static constexpr bool kAlo = SPLIT3 && !TA && (2 * kMmaN + 2 * BK <= 512);
+  static constexpr int kLoFit = (200 * 1024 - 6 * kStage) / kBBytes;  // keep >= 6 raw stages
+  static constexpr int kLoTmem0 = kAlo ? (512 - 2 * kMmaN) / BK : 2;
+  static constexpr int kLoTmem = kLoTmem0 < kLoFit ? kLoTmem0 : (kLoFit < 2 ? 2 : kLoFit);
+  // ready/empty_lo ring depth (only pacing barriers, no storage, for 1xTF32)
+  static constexpr int kLo = !SPLIT3 ? 8 : kAlo ? (kLoTmem < 8 ? kLoTmem : 8) : 2;
+  static constexpr int kLoBytes = SPLIT3 ? kLo * (kAlo ? kBBytes : kStage) : 0;
+  static constexpr int kRawFit = (200 * 1024 - kLoBytes) / kStage;
+  static constexpr int kRaw = kRawFit < 12 ? kRawFit : 12;
   static constexpr int kTileM = kMmaM;
   static constexpr int kTileN = kMmaN;
   static constexpr int kCols = kMmaN / 2;            // columns per promotion warp
   static constexpr int kRawBytes = kRaw * kStage;
-  static constexpr int kLoBytes = SPLIT3 ? kLo * kStage : 0;
   static constexpr int kNumBars = 2 * kRaw + 2 * kLo + 4;
   static constexpr int kEpiStageBytes = kEpiWarps * 32 * kEpiStride * 4;  // transpose staging
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kRawBytes + kLoBytes + kEpiStageBytes + kNumBars * 8 + 16;
@@ -295,7 +305,7 @@ __device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, 
 template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB, int BK = 32, bool CONV = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
-  using Cfg = TcCfg<CG, BN_CTA, SPLIT3, BK>;
+  using Cfg = TcCfg<CG, BN_CTA, SPLIT3, BK, TA>;
   static_assert(BK == 32 || BK == 16, "BK");
   static_assert(BK == 32 || (!TA && TB), "64-B rows only for K-major operands");
   static_assert(TB || BN_CTA % 32 == 0, "MN-major B needs 32-column atoms");
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // write and read.  Needs K-major A and free TMEM columns beyond the two
   // partial accumulators (not the 2-CTA 256-column tile, whose partials use
   // all 512 columns).
-  constexpr bool ALO = SPLIT3 && !TA && (2 * Cfg::kMmaN + LO * BK <= 512);
+  constexpr bool ALO = Cfg::kAlo;
   constexpr int kTmemNeed = 2 * Cfg::kMmaN + (ALO ? LO * BK : 0);
   constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
   constexpr uint32_t kAloCol = 2 * Cfg::kMmaN;  // first TMEM column of the A_lo stages
@@ -316,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* rawA = smem;
   uint8_t* rawB = rawA + RAW * Cfg::kABytes;
   uint8_t* loA = rawB + RAW * Cfg::kBBytes;
-  uint8_t* loB = loA + (SPLIT3 ? LO * Cfg::kABytes : 0);
+  uint8_t* loB = loA + ((SPLIT3 && !ALO) ? LO * Cfg::kABytes : 0);
   float* epi_stage = reinterpret_cast<float*>(smem + Cfg::kRawBytes + Cfg::kLoBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRawBytes + Cfg::kLoBytes + Cfg::kEpiStageBytes);
   uint64_t* full = bars;                   // [RAW] TMA landed (local)
@@ -363,16 +373,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp < 4) {
     ptx::setmaxnreg_dec<80>();  // producer / MMA / allocator warpgroup
-    if (warp == 0) {
-      // ---------------------------------------------------------- producer
+    if (warp != 1) {
+      // ---------------------------------------------------------- producers
+      // Warps 0, 2, 3 (one lane each) take every third K-iteration: a single
+      // issuing thread lands at most about one TMA load per ~0.3 us
+      // (scripts/tma_probe.py), which bounds skinny tiles whose stages carry
+      // little MMA work; three issuers triple that rate.
+      const int pi = warp == 0 ? 0 : warp - 1;
       if (ptx::elect_one()) {
-        int s = 0;
+        int s = 0, own = 0;
         uint32_t ph = 0;
         UnitIter ui = units_begin(p, cluster_id, num_clusters);
         Unit u;
         int wi = 0;
         while (units_next(p, num_clusters, ui, u)) {
-          if (p.wave_ctr && wi >= 1 && wi < p.full_waves) {
+          if (pi == 0 && p.wave_ctr && wi >= 1 && wi < p.full_waves) {
             // Keep the persistent clusters in step at tile boundaries so the
             // concurrently live tiles keep sharing A/B panels in L2.
             atomicAdd(p.wave_ctr, 1u);
@@ -386,49 +401,52 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int col0 = tni * Cfg::kTileN + static_cast<int>(rank) * BN_CTA;
           const int rows_here = min(kBMCta, p.m - row0);
           for (int kb = u.kb0; kb < u.kb1; ++kb) {
-            if (kb == max(u.kb0, u.kb1 - p.kc_blocks) && u.kb1 == p.kblocks && p.beta != 0.0f && rows_here > 0) {
-              // This unit's epilogue will read beta*C: stage this CTA's C rows
-              // in L2 about one K_c chunk (plus the ring depth) ahead, so the
-              // epilogue's loads hit L2 instead of exposing DRAM latency.
-              const int c0 = tni * Cfg::kTileN;
-              const int cols = min(Cfg::kTileN, p.n - c0);
-              const uint32_t bytes = static_cast<uint32_t>(cols * 4) & ~15u;  // floor: never past the row
-              if (bytes)
-                for (int r = 0; r < rows_here; ++r) ptx::prefetch_l2_bulk(p.C + (row0 + r) * p.ldc + c0, bytes);
-            }
-            ptx::mbar_wait(&empty_raw[s], ph ^ 1);
-            ptx::mbar_arrive_expect_tx(&full[s], Cfg::kABytes + Cfg::kBBytes);
-            if constexpr (CONV) {
-              // K-block kb = (filter tap, BK-channel chunk).  Output pixel row0
-              // = (b, y, x); its input window starts at (y - pad, x - pad) and
-              // the tap adds (ky, kx) as im2col offsets.  TMA walks 128 output
-              // pixels in W, H, N order and zero-fills outside the image.
-              const int chunks = p.cv_c / BK;
-              const int tap = kb / chunks, c0 = (kb - tap * chunks) * BK;
-              const int ky = tap / p.cv_s, kx = tap - ky * p.cv_s;
-              const int hw = p.cv_ho * p.cv_wo;
-              const int b = row0 / hw, yx = row0 - b * hw;
-              const int y = yx / p.cv_wo, x = yx - y * p.cv_wo;
-              ptx::tma_load_im2col_4d(rawA + s * Cfg::kABytes, &tmA, &full[s], c0, x - p.cv_pad, y - p.cv_pad, b,
-                                      static_cast<uint16_t>(kx), static_cast<uint16_t>(ky));
-            } else if constexpr (!TA) {  // A: one K-major box BK (k) x 128 (rows)
-              ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * BK, row0);
-            } else {              // A^T: four MN-major boxes 32 (rows) x 32 (k)
+            if (own == pi) {
+              if (kb == max(u.kb0, u.kb1 - p.kc_blocks) && u.kb1 == p.kblocks && p.beta != 0.0f && rows_here > 0) {
+                // This unit's epilogue will read beta*C: stage this CTA's C rows
+                // in L2 about one K_c chunk (plus the ring depth) ahead, so the
+                // epilogue's loads hit L2 instead of exposing DRAM latency.
+                const int c0 = tni * Cfg::kTileN;
+                const int cols = min(Cfg::kTileN, p.n - c0);
+                const uint32_t bytes = static_cast<uint32_t>(cols * 4) & ~15u;  // floor: never past the row
+                if (bytes)
+                  for (int r = 0; r < rows_here; ++r) ptx::prefetch_l2_bulk(p.C + (row0 + r) * p.ldc + c0, bytes);
+              }
+              ptx::mbar_wait(&empty_raw[s], ph ^ 1);
+              ptx::mbar_arrive_expect_tx(&full[s], Cfg::kABytes + Cfg::kBBytes);
+              if constexpr (CONV) {
+                // K-block kb = (filter tap, BK-channel chunk).  Output pixel row0
+                // = (b, y, x); its input window starts at (y - pad, x - pad) and
+                // the tap adds (ky, kx) as im2col offsets.  TMA walks 128 output
+                // pixels in W, H, N order and zero-fills outside the image.
+                const int chunks = p.cv_c / BK;
+                const int tap = kb / chunks, c0 = (kb - tap * chunks) * BK;
+                const int ky = tap / p.cv_s, kx = tap - ky * p.cv_s;
+                const int hw = p.cv_ho * p.cv_wo;
+                const int b = row0 / hw, yx = row0 - b * hw;
+                const int y = yx / p.cv_wo, x = yx - y * p.cv_wo;
+                ptx::tma_load_im2col_4d(rawA + s * Cfg::kABytes, &tmA, &full[s], c0, x - p.cv_pad, y - p.cv_pad, b,
+                                        static_cast<uint16_t>(kx), static_cast<uint16_t>(ky));
+              } else if constexpr (!TA) {  // A: one K-major box BK (k) x 128 (rows)
+                ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * BK, row0);
+              } else {              // A^T: four MN-major boxes 32 (rows) x 32 (k)
 #pragma unroll
-              for (int j = 0; j < kBMCta / 32; ++j)
-                ptx::tma_load_2d(rawA + s * Cfg::kABytes + j * 4096, &tmA, &full[s], row0 + 32 * j, kb * BK);
-            }
-            if constexpr (!TB) {  // B: BN_CTA/32 MN-major boxes 32 (cols) x 32 (k)
+                for (int j = 0; j < kBMCta / 32; ++j)
+                  ptx::tma_load_2d(rawA + s * Cfg::kABytes + j * 4096, &tmA, &full[s], row0 + 32 * j, kb * BK);
+              }
+              if constexpr (!TB) {  // B: BN_CTA/32 MN-major boxes 32 (cols) x 32 (k)
 #pragma unroll
-              for (int j = 0; j < BN_CTA / 32; ++j)
-                ptx::tma_load_2d(rawB + s * Cfg::kBBytes + j * 4096, &tmB, &full[s], col0 + 32 * j, kb * BK);
-            } else {              // B^T: one K-major box BK (k) x BN_CTA (cols)
-              ptx::tma_load_2d(rawB + s * Cfg::kBBytes, &tmB, &full[s], kb * BK, col0);
+                for (int j = 0; j < BN_CTA / 32; ++j)
+                  ptx::tma_load_2d(rawB + s * Cfg::kBBytes + j * 4096, &tmB, &full[s], col0 + 32 * j, kb * BK);
+              } else {              // B^T: one K-major box BK (k) x BN_CTA (cols)
+                ptx::tma_load_2d(rawB + s * Cfg::kBBytes, &tmB, &full[s], kb * BK, col0);
+              }
             }
+            if (++own == kProducers) own = 0;
             if (++s == RAW) { s = 0; ph ^= 1; }
           }
         }
-        trace_mark(p, 2);  // producer done issuing
+        if (pi == 0) trace_mark(p, 2);  // producer done issuing
       }
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
@@ -702,7 +720,7 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, 
 template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB, int BK, bool CONV>
 tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams p, int num_sms, bool streamk,
                         cudaStream_t stream) {
-  using Cfg = TcCfg<CG, BN_CTA, SPLIT3, BK>;
+  using Cfg = TcCfg<CG, BN_CTA, SPLIT3, BK, TA>;
   auto kern = k_sgemm_tc<CG, BN_CTA, SPLIT3, TA, TB, BK, CONV>;
   static bool attr_set = false;  // per instantiation; attribute is per-function, process-wide
   if (!attr_set) {
@@ -738,9 +756,11 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
   p.full_waves = 0;
   // Wave barrier (default on; TM_WAVE_SYNC=0 disables): measured on C5 it cuts
   // DRAM traffic 35 -> 22 GB per launch and, under the power cap, raises the
-  // sustained clock and throughput by ~10%.
+  // sustained clock and throughput by ~10%.  Only for long K loops: with short
+  // tiles (C4, the convolution: <= 18 K-blocks) there is little panel reuse to
+  // protect and the per-tile grid-wide barrier costs 10-20%.
   static const bool wave_sync = [] { const char* e = std::getenv("TM_WAVE_SYNC"); return !(e && e[0] == '0'); }();
-  if (wave_sync && !p.streamk && p.num_tiles / clusters >= 2) {
+  if (wave_sync && !CONV && p.kblocks >= 64 && !p.streamk && p.num_tiles / clusters >= 2) {
     float* ws_unused = nullptr;
     unsigned epoch_unused = 0;
     tm_status st = streamk_workspace(stream, 0, 1, &ws_unused, &p.wave_ctr, &epoch_unused);  // slot 0
