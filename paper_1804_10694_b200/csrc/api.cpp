@@ -310,6 +310,15 @@ tm_status tm_conv2d_nhwc(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f,
                        r <= 128 && s <= 128;
     if (algo == TM_ALGO_TF32X3 && !tc_ok) return TM_ERR_INVALID_VALUE;
     if (algo == TM_ALGO_SIMT_F32 || !tc_ok) return tmk::launch_conv_simt(a, stream);
+    // "direct" / "im2col" -- tests and bench only
+    const char* conv_path = std::getenv("TM_CONV_PATH");
+    const bool force_im2col = conv_path && std::strcmp(conv_path, "im2col") == 0;
+    if (!force_im2col && tmk::conv_direct_fits(a)) {
+      if (tmk::log_enabled())
+        std::fprintf(stderr, "[tm] conv P=%lld F=%lld K=%lld -> tf32x3 direct\n",
+                     static_cast<long long>(P), static_cast<long long>(f), static_cast<long long>(r * s * c));
+      return tmk::launch_conv_direct(a, dev->sms, stream);
+    }
     const int bk = (c % 32 == 0) ? 32 : 16;
     int cg = 1, bn = 16;
     if (f <= 16) { cg = 1; bn = 16; }

@@ -72,6 +72,10 @@ struct ConvArgs {
 // bk: channels per stage (16 or 32); cg/bn as TcChoice.
 tm_status launch_conv_tc(const ConvArgs& a, int cg, int bn, int bk, bool streamk, int num_sms, cudaStream_t stream);
 tm_status launch_conv_simt(const ConvArgs& a, cudaStream_t stream);
+// Direct (halo-tile) tensor-core convolution for C % 16 == 0, F <= 64 and
+// filters that fit in shared memory (tc_conv_direct.cu).
+bool conv_direct_fits(const ConvArgs& a);
+tm_status launch_conv_direct(const ConvArgs& a, int num_sms, cudaStream_t stream);
 
 // Picks the tensor-core configuration for a shape (planner, plan.cpp).
 TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms);

@@ -1,7 +1,8 @@
-"""Implicit-GEMM convolution (tm_conv2d_nhwc, the
-paper's Conv benchmark PAPER.md:824-826) against the convolution oracle
-(pinned in test_conv_oracle.py): tensor-core path (TMA im2col), every compiled
-configuration, and the SIMT direct-convolution path."""
+"""Convolution (tm_conv2d_nhwc, the paper's Conv
+benchmark PAPER.md:824-826) against the convolution oracle (pinned in
+test_conv_oracle.py): the direct halo-tile tensor-core kernel (default where it
+fits), the implicit-GEMM tensor-core kernel (TMA im2col; every compiled
+configuration), and the SIMT direct-convolution path."""
 import os
 
 import numpy as np
@@ -15,7 +16,7 @@ TOL = 1e-5
 TF32X3, SIMT, AUTO = 1, 2, 0
 
 
-def _run(shape, algo=AUTO, beta=0.5, config=None, seed=0, kind="uniform"):
+def _run(shape, algo=AUTO, beta=0.5, config=None, seed=0, kind="uniform", path=None):
     import torch
     import paper_1804_10694_b200 as tm
     Nb, H, W, C, F, R, S, pad = shape
@@ -28,11 +29,15 @@ def _run(shape, algo=AUTO, beta=0.5, config=None, seed=0, kind="uniform"):
     dX, dW, dY = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (X, Wt, Y0))
     if config:
         os.environ["TM_CONV_CONFIG"] = config
+        path = "im2col"
+    if path:
+        os.environ["TM_CONV_PATH"] = path
     try:
         tm.conv2d_nhwc(dX, dW, dY, 1.5, beta, pad, algo=algo)
         torch.cuda.synchronize()
     finally:
         os.environ.pop("TM_CONV_CONFIG", None)
+        os.environ.pop("TM_CONV_PATH", None)
     return X, Wt, Y0, dY.cpu().numpy().reshape(-1, F)
 
 
@@ -40,10 +45,10 @@ SHAPES = [(2, 9, 11, 16, 16, 3, 3, 1), (1, 7, 6, 16, 16, 3, 3, 0), (2, 13, 10, 3
           (1, 8, 8, 16, 32, 7, 7, 3), (3, 20, 17, 64, 48, 1, 1, 0), (1, 33, 35, 16, 8, 5, 3, 1)]
 
 
-@pytest.mark.parametrize("algo", [AUTO, SIMT])
+@pytest.mark.parametrize("algo,path", [(AUTO, None), (AUTO, "im2col"), (SIMT, None)])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_conv_parity(algo, shape):
-    X, Wt, Y0, Y = _run(shape, algo)
+def test_conv_parity(algo, path, shape):
+    X, Wt, Y0, Y = _run(shape, algo, path=path)
     R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, shape[-1])
     assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL
 
@@ -58,20 +63,39 @@ def test_conv_tensor_core_configs(config, shape):
     assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL
 
 
-def test_conv_beta_zero_and_integer_bit_exact():
-    shape = (2, 12, 12, 16, 16, 3, 3, 1)
-    X, Wt, Y0, Y = _run(shape, TF32X3, beta=0.0)
+# Direct kernel geometry: several 128-pixel tiles per output row with a ragged
+# last one, tiles crossing image boundaries, 16/32/48/64 channels (one to
+# three halo boxes, 64-B and 128-B swizzled rows), F below / at / above a
+# power of two, 1x1 .. 5x5 taps with and without padding, one-pixel rows.
+DIRECT_SHAPES = [(2, 6, 300, 16, 16, 3, 3, 1), (3, 5, 128, 16, 16, 3, 3, 1), (1, 4, 257, 32, 32, 3, 3, 1),
+                 (2, 5, 140, 48, 20, 3, 3, 1), (1, 4, 130, 64, 64, 3, 3, 1), (2, 7, 150, 16, 8, 5, 5, 2),
+                 (2, 6, 131, 16, 40, 1, 1, 0), (1, 9, 200, 32, 16, 3, 5, 0), (2, 3, 1, 16, 16, 3, 3, 1),
+                 (1, 40, 3, 16, 12, 3, 1, 1)]
+
+
+@pytest.mark.parametrize("shape", DIRECT_SHAPES)
+def test_conv_direct_parity(shape):
+    X, Wt, Y0, Y = _run(shape, TF32X3)
+    R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, shape[-1])
+    assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL
+
+
+@pytest.mark.parametrize("path", [None, "im2col"])
+def test_conv_beta_zero_and_integer_bit_exact(path):
+    shape = (2, 12, 140, 16, 16, 3, 3, 1)
+    X, Wt, Y0, Y = _run(shape, TF32X3, beta=0.0, path=path)
     R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.0, None, 1)
     assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL
-    X, Wt, Y0, Y = _run(shape, TF32X3, kind="integer")
+    X, Wt, Y0, Y = _run(shape, TF32X3, kind="integer", path=path)
     R, _ = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, 1)
     assert np.array_equal(Y.astype(np.float64), R)
 
 
-def test_conv_paper_shape_sampled_pixels():
+@pytest.mark.parametrize("path", [None, "im2col"])
+def test_conv_paper_shape_sampled_pixels(path):
     """512x512 input, 16 input/output features, batch 32, 3x3."""
     shape = (32, 512, 512, 16, 16, 3, 3, 1)
-    X, Wt, Y0, Y = _run(shape, AUTO, seed=1808)
+    X, Wt, Y0, Y = _run(shape, AUTO, seed=1808, path=path)
     P = Y.shape[0]
     g = si.rng(5)
     pix = np.unique(np.concatenate([g.integers(0, P, 3000), [0, 511, 512, 512 * 511, P - 1, P - 512]]))
