@@ -153,6 +153,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < boxes; ++i)
               ptx::tma_load_4d(halo + slot * p.slot_bytes + i * p.box_bytes, &tmX, &halo_full[slot], i * p.cw,
                                x0 - p.pad, y - p.pad, b);
+            if (p.beta != 0.0f) {
+              // the epilogue will read beta * Y for this tile's outputs (one
+              // contiguous run of the output row): stage it in L2 now, the
+              // halo ring depth ahead of its use
+              const int cnt = min(4 * p.ow, p.wo - x0);
+              ptx::prefetch_l2_bulk(p.Y + static_cast<long long>((b * p.ho + y) * p.wo + x0) * p.f,
+                                    static_cast<uint32_t>(cnt * p.f * 4));
+            }
           }
           if (++own == kDcProducers) own = 0;
           if (++slot == p.n_slots) { slot = 0; ph ^= 1; }
