@@ -111,18 +111,21 @@ tm_status tm_sgemm_colmajor(char transa, char transb, int64_t m, int64_t n, int6
                             const float* A, int64_t lda, const float* B, int64_t ldb,
                             float beta, float* C, int64_t ldc, void* stream);
 
-/* Implicit-GEMM 2-D convolution (the paper's Conv
- * benchmark, implemented as sgemm): stride 1, dilation 1,
+/* 2-D convolution as a GEMM (the paper's Conv
+ * benchmark, "sgemm ... used to implement convolutions"):
+ * stride 1, dilation 1,
  * zero padding `pad`, device pointers
  *   X  : nb x h x w x c        (NHWC, dense)
  *   Wt : f x r x s x c         (KRSC filters, dense)
  *   Y  : nb x ho x wo x f      (NHWC, dense), ho = h + 2 pad - r + 1, wo = w + 2 pad - s + 1
  *   Y[b,y,x,f] = alpha * sum_{ky,kx,c} X[b, y+ky-pad, x+kx-pad, c] * Wt[f,ky,kx,c] + beta * Y[b,y,x,f]
- * (X outside the image reads as zero).  AUTO uses the 3xTF32 tensor-core path
- * (A = im2col of X streamed by TMA im2col-mode copies, never materialised)
- * when c % 16 == 0, f % 4 == 0, pointers 16-byte aligned and pad <= 127, else
- * the FP32 SIMT direct convolution; TM_ALGO_TF32X3 on other shapes returns
- * TM_ERR_INVALID_VALUE.  Same accuracy contract (normalised by
+ * (X outside the image reads as zero).  AUTO uses a 3xTF32 tensor-core path
+ * when c % 16 == 0, f % 4 == 0, pointers 16-byte aligned and pad <= 127 --
+ * the direct halo-tile kernel when s is 1 or 3, r * c <= 128 and f <= 64
+ * (filters resident in shared memory), else the implicit-GEMM kernel (A =
+ * im2col of X streamed by TMA im2col-mode copies, never materialised) -- and
+ * otherwise the FP32 SIMT direct convolution; TM_ALGO_TF32X3 on shapes
+ * outside the tensor-core rule returns TM_ERR_INVALID_VALUE.  Same accuracy contract (normalised by
  * |alpha| sum |X||Wt| + |beta||Y|), special cases and errors as tm_sgemm_ex. */
 tm_status tm_conv2d_nhwc(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f, int64_t r, int64_t s,
                          int64_t pad, float alpha, const float* X, const float* Wt, float beta, float* Y,
