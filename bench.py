@@ -387,14 +387,19 @@ def run_conv(args):
     algo_bytes = 4 * (X.numel() + Wt.numel() + (2 if beta != 0.0 else 1) * Y.numel())
     peaks = load_peaks()
     gbs = algo_bytes / (ms * 1e-3) / 1e9
-    line = {"metric": "conv2d (implicit GEMM) GB/s and GFLOP/s", "value": round(gbs, 2), "unit": "GB/s",
+    traffic, traffic_src = (ncu_traffic("CONV", "tf32x3", 1) if (beta == 0.0 and algo != 2) else (None, None))
+    line = {"metric": "conv2d GB/s (PAPER.md:826 Conv shape, 3xTF32 tensor cores)", "value": round(gbs, 2), "unit": "GB/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "dtype": "f32 (3xTF32 tensor-core)" if algo != 2 else "f32",
             "gflops": round(flops / (ms * 1e-3) / 1e9, 1), "data": "synthetic (device-generated U[-1,1))",
             "config": {"workload": f"PAPER.md:826 Conv: NHWC 32x512x512x16, KRSC 16x3x3x16, pad 1, alpha {alpha} beta {beta}",
                        "l2": "inputs larger than L2, no flush"},
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": None},
+                         "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
+                         "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
+                         "algorithmic_bytes": algo_bytes,
+                         "kernel": "k_conv_direct (auto)" if algo != 2 else "k_conv_simt"},
+            "gpu_launches": args.steps,
             "clocks": clocks.summary()}
     print(json.dumps(line), flush=True)
     return 0
