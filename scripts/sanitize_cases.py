@@ -1,5 +1,6 @@
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck):
-every path on partial tiles, transposes, stream-K, beta = 0 and alpha = 0."""
+every path on partial tiles, transposes, stream-K, beta = 0 and alpha = 0,
+and the three convolution kernels."""
 import os, sys
 import numpy as np
 import torch
@@ -29,5 +30,20 @@ for (m, n, k) in cases:
         del os.environ["TM_TC_CONFIG"]
     A, B, C = t(m, k), t(k, n), t(m, n)
     tm.sgemm_ex(A, B, C, 0.0, 0.5, 0)
+# convolution: direct (S in {1, 3}), implicit-GEMM (forced and S = 5), SIMT; ragged rows, beta 0 / 0.5
+for (nb, h, w, c, f, r, s, pad) in [(2, 5, 140, 16, 16, 3, 3, 1), (1, 4, 130, 32, 24, 3, 3, 1),
+                                     (2, 3, 131, 16, 40, 1, 1, 0), (1, 6, 37, 16, 8, 5, 5, 2),
+                                     (1, 5, 20, 48, 20, 3, 3, 1)]:
+    ho, wo = h + 2 * pad - r + 1, w + 2 * pad - s + 1
+    X, Wt = torch.rand((nb, h, w, c), generator=g, device="cuda"), torch.rand((f, r, s, c), generator=g, device="cuda")
+    for path in (None, "im2col"):
+        for beta in (0.5, 0.0):
+            if path:
+                os.environ["TM_CONV_PATH"] = path
+            Y = torch.rand((nb, ho, wo, f), generator=g, device="cuda")
+            tm.conv2d_nhwc(X, Wt, Y, 1.5, beta, pad)
+            os.environ.pop("TM_CONV_PATH", None)
+    Y = torch.rand((nb, ho, wo, f), generator=g, device="cuda")
+    tm.conv2d_nhwc(X, Wt, Y, 1.5, 0.5, pad, algo=2)
 torch.cuda.synchronize()
 print("sanitize cases done")
