@@ -28,10 +28,11 @@
 //   warps 0, 2     halo producers (one lane each, alternate tiles); warp 0
 //                  also loads the filters once.  Warp 2 allocates TMEM.
 //   warp 1         MMA issuer (one lane).
-//   warps 4-11     split, two warpgroups taking alternate tiles: halo ->
-//                  (hi | lo) TMEM A slots, one slot per tile.
-//   warps 12-15    promotion, shift-add and epilogue (tc_gemm.cuh epi_store:
-//                  alpha / beta, full / partial tile separation).
+//   warps 4-7      split: halo -> (hi | lo) TMEM A slots, one slot per tile.
+//   warps 8-15     promotion, shift-add and epilogue, two warpgroups, one per
+//                  TMEM accumulator (tc_gemm.cuh epi_store: alpha / beta,
+//                  full / partial tile separation).  The epilogue is the
+//                  longest per-tile chain, hence two groups.
 #include "tc_gemm.cuh"
 
 namespace tmk {
@@ -39,14 +40,13 @@ namespace {
 
 constexpr int kDcBK = 16;            // channels per stage (one 64-B row of a filter box)
 constexpr int kDcLanes = 128;        // halo pixels per tile = TMEM lanes
-constexpr int kDcSplitWarps = 8;     // two split warpgroups
-constexpr int kDcEpiWarps = 4;       // promotion / epilogue warpgroup
+constexpr int kDcSplitWarps = 4;     // one split warpgroup
+constexpr int kDcEpiWarps = 8;       // two promotion / epilogue warpgroups (one per accumulator)
 constexpr int kDcMaxSlots = 4;       // TMEM A slots (one tile each)
 constexpr int kDcMaxSmem = 227 * 1024;
-// Halo producers and split groups both alternate tiles by parity and the halo
-// ring depth is even, so every ring slot is always filled by the same producer
-// and drained by the same split group: each slot's phases then complete in
-// order, which the parity waits rely on.
+// The halo producers alternate tiles by parity and the halo ring depth is
+// even, so every ring slot is always filled by the same producer: each slot's
+// phases then complete in order, which the parity waits rely on.
 constexpr int kDcProducers = 2;
 
 struct DcParams {
@@ -103,15 +103,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(bres_full, 1);
     for (int i = 0; i < p.n_slots; ++i) {
       ptx::mbar_init(&halo_full[i], 1);
-      ptx::mbar_init(&halo_empty[i], kDcSplitWarps / 2);  // the tile's split group
+      ptx::mbar_init(&halo_empty[i], kDcSplitWarps);
     }
     for (int i = 0; i < kDcMaxSlots; ++i) {
-      ptx::mbar_init(&ready[i], kDcSplitWarps / 2);
+      ptx::mbar_init(&ready[i], kDcSplitWarps);
       ptx::mbar_init(&a_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&part_full[i], 1);
-      ptx::mbar_init(&part_empty[i], kDcEpiWarps);
+      ptx::mbar_init(&part_empty[i], kDcEpiWarps / 2);  // the accumulator's epilogue group
     }
     ptx::fence_mbarrier_init();
   }
@@ -199,13 +199,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++pb == p.n_part) { pb = 0; pph ^= 1; }
       }
     }
-  } else if (warp < 12) {
+  } else if (warp < 8) {
     // -------------------------------------------------------------- split
-    // two groups (warps 4-7, 8-11) take alternate tiles; both keep the
-    // launch's 128 registers: (80 + 2 * 128) * 128 + 176 * 128 = 65536
-    const int g = (warp - 4) >> 2;
+    // keeps the launch's 128 registers: (80 + 128) * 128 + 152 * 256 = 65536
     const int q = warp & 3;
-    if (g == 0) {
+    {
       // resident filters: lo = split of hi, same layout (elementwise)
       const int st = q * 32 + lane;
       ptx::mbar_wait(bres_full, 0);
@@ -221,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int slot = 0, sl = 0, i = 0;
     uint32_t ph = 0, phl = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
-      if ((i & 1) == g) {
+      {
         ptx::mbar_wait(&halo_full[slot], ph);
         ptx::mbar_wait(&a_empty[sl], phl ^ 1);
         ptx::tc_fence_after();
@@ -264,12 +262,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // -------------------------------------------------------------- promotion, shift-add, epilogue
-    ptx::setmaxnreg_inc<176>();
+    // Group e (warps 8-11, 12-15) drains accumulator e: with two accumulators
+    // the groups alternate tiles, with one only group 0 works.
+    ptx::setmaxnreg_inc<152>();
     const int q = warp & 3;
-    float* stage = epi_stage + (warp - 12) * 32 * kEpiStride;
-    int pb = 0;
+    const int e = (warp - 8) >> 2;
+    float* stage = epi_stage + (warp - 8) * 32 * kEpiStride;
+    const int pb = e;
     uint32_t pph = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    int i = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
+      if (i % p.n_part != e) continue;
       ptx::mbar_wait(&part_full[pb], pph);
       ptx::tc_fence_after();
       int b, y, x0;
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (valid > 0 && f0 < p.f)
           epi_store<16>(p.Y, p.f, row0 + valid, p.f, row0, f0, acc, p.alpha, p.beta, stage, lane);
       }
-      if (++pb == p.n_part) { pb = 0; pph ^= 1; }
+      pph ^= 1;
     }
   }
 
