@@ -43,6 +43,7 @@ constexpr int kDcLanes = 128;        // halo pixels per tile = TMEM lanes
 constexpr int kDcSplitWarps = 4;     // one split warpgroup
 constexpr int kDcEpiWarps = 8;       // two promotion / epilogue warpgroups (one per accumulator)
 constexpr int kDcMaxSlots = 4;       // TMEM A slots (one tile each)
+constexpr int kDcMaxStages = 8;      // R * C / 16 (K = R * C <= 128)
 constexpr int kDcMaxSmem = 227 * 1024;
 // The halo producers alternate tiles by parity and the halo ring depth is
 // even, so every ring slot is always filled by the same producer: each slot's
@@ -216,6 +217,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool cw16 = p.cw == 16;  // 64-B halo rows (SWIZZLE_64B), else 128-B rows (SWIZZLE_128B)
     const int rb = p.cw * 4;
     const int hp = p.ow * q + lane;  // this lane's halo pixel
+    // Per-stage shared-memory offsets of this lane's 16 channels inside a halo
+    // slot (tile-independent): stage s = (ky, 16-channel chunk ci).  TMA
+    // swizzle (box bases 1 KiB aligned): 16-B chunk j of a row is stored at
+    // j ^ ((row / 2) % 4) for 64-B rows, j ^ (row % 8) for 128-B rows.
+    uint32_t soff[kDcMaxStages], sxor[kDcMaxStages];
+#pragma unroll
+    for (int s = 0; s < kDcMaxStages; ++s) {
+      const int ky = s / p.chunks, ci = s - ky * p.chunks;
+      const int box = cw16 ? ci : (ci >> 1);
+      const int within = cw16 ? 0 : ((ci & 1) << 2);  // first 16-B chunk of these 16 channels
+      const int row = ky * p.halo_w + hp;             // pixel row inside the box
+      soff[s] = static_cast<uint32_t>(box * p.box_bytes + row * rb);
+      sxor[s] = static_cast<uint32_t>(cw16 ? ((row >> 1) & 3) : (row & 7));
+      sxor[s] = (sxor[s] ^ static_cast<uint32_t>(within)) & 7u;  // within in {0, 4} and j < 4: (within + j) ^ sw = (j ^ (sw ^ within))
+    }
     int slot = 0, sl = 0, i = 0;
     uint32_t ph = 0, phl = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
@@ -225,25 +241,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         const uint32_t hb = halo_s + slot * p.slot_bytes;
         const uint32_t ta = trow + static_cast<uint32_t>(sl * p.a_cols);
-        for (int s = 0; s < p.stages; ++s) {
-          const int ky = s / p.chunks, ci = s - ky * p.chunks;
-          const int box = cw16 ? ci : (ci >> 1);
-          const int within = cw16 ? 0 : ((ci & 1) << 2);  // first 16-B chunk of these 16 channels
-          const int row = ky * p.halo_w + hp;             // pixel row inside the box
-          const uint32_t rowp = hb + box * p.box_bytes + row * rb;
-          // TMA swizzle (box bases 1 KiB aligned): 16-B chunk j of a row is
-          // stored at j ^ ((row / 2) % 4) for 64-B rows, j ^ (row % 8) for 128-B rows.
-          const int sw = cw16 ? ((row >> 1) & 3) : (row & 7);
+#pragma unroll
+        for (int s = 0; s < kDcMaxStages; ++s) {
+          if (s >= p.stages) break;
+          const uint32_t rowp = hb + soff[s];
           uint4 v[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) v[j] = ptx::lds128(rowp + (((within + j) ^ sw) << 4));
+          for (int j = 0; j < 4; ++j) v[j] = ptx::lds128(rowp + ((static_cast<uint32_t>(j) ^ sxor[s]) << 4));
           uint32_t hl[32];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t x[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              hl[4 * j + e] = x[e] & 0xFFFFE000u;             // A_hi (what kind::tf32 reads)
+              hl[4 * j + e] = x[e];                           // A_hi: kind::tf32 truncates the raw value
               hl[kDcBK + 4 * j + e] = tf32_lo_bits(x[e]);     // A_lo
             }
           }
