@@ -150,6 +150,42 @@ const char* tm_status_string(tm_status s);
 /* Library version as major*10000 + minor*100 + patch. */
 int tm_get_version(void);
 
+/* Measured configuration choice (the paper auto-tuned
+ * its sgemm's tile sizes).  Times every compiled 3xTF32
+ * tensor-core configuration -- 1- or 2-SM CTA group x 32/64/128-column CTA
+ * tile x data-parallel/stream-K schedule -- on these operands (op(A), op(B) as
+ * in tm_sgemm_op; `reps` timed runs each after one warm-up, median kept) and
+ * records the fastest in a process-wide cache keyed by (m, n, k, opa, opb,
+ * beta != 0, SM count); later AUTO/TF32X3 calls with that key use it.  The
+ * trials write a library-allocated scratch copy of C: the caller's C is only
+ * read (when beta != 0) and is unchanged.  Device pointers, stream-ordered
+ * but synchronising (it reads the timings).  Outputs (may be NULL): the chosen
+ * cg (1/2), bn_cta (32/64/128), streamk (0/1) and its median time in ms.
+ * Errors: TM_ERR_INVALID_VALUE if tm_sgemm_op(..., TM_ALGO_TF32X3) would reject
+ * the arguments, if m, n or k is 0, alpha == 0 or reps is outside [1, 1000];
+ * TM_ERR_CUDA on allocation or launch failure. */
+tm_status tm_sgemm_tune(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda,
+                        const float* B, int64_t ldb, float beta, const float* C, int64_t ldc, void* stream, int reps,
+                        int* best_cg, int* best_bn, int* best_streamk, float* best_ms);
+
+/* Tuning cache management (host-only).  File format: one entry per line,
+ * "m n k opa opb beta_nonzero sms cg bn_cta streamk" ('#' lines are comments);
+ * load skips malformed entries and returns how many it added (-1 if the file
+ * cannot be opened); save overwrites `path`. */
+int tm_tune_cache_size(void);
+tm_status tm_tune_cache_clear(void);
+tm_status tm_tune_cache_save(const char* path);
+int tm_tune_cache_load(const char* path);
+
+/* The plan tm_sgemm_op(opa, opb, ..., algo) would use (host-only, no launch):
+ * *path = 0 invalid, 1 no-op, 2 scale, 3 tensor cores, 4 SIMT; for tensor
+ * cores the CTA group, CTA tile width and schedule (tuned entry if cached,
+ * else the cost model).  Output pointers may be NULL.  Returns
+ * TM_ERR_INVALID_VALUE for arguments the call would reject. */
+tm_status tm_sgemm_plan_config(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
+                               int64_t lda, const float* B, int64_t ldb, float beta, const float* C, int64_t ldc,
+                               int algo, int* path, int* cg, int* bn_cta, int* streamk);
+
 /* Name of the path tm_sgemm_ex would take for these arguments on the current
  * device ("tf32x3", "simt", "scale", "noop", or "invalid"); host-only, no launch. */
 const char* tm_sgemm_plan_name(int64_t m, int64_t n, int64_t k, float alpha,

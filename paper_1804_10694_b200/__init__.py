@@ -15,7 +15,8 @@ import os
 
 __all__ = [
     "ALGO_AUTO", "ALGO_TF32X3", "ALGO_SIMT_F32", "ALGO_TF32X1", "TmError", "lib", "lib_path", "sgemm",
-    "sgemm_ex", "sgemm_host", "plan_name", "dist_rows", "Comm", "status_string", "EXPORTED_SYMBOLS",
+    "sgemm_ex", "sgemm_host", "plan_name", "plan_config", "tune", "tune_cache_save", "tune_cache_load",
+    "tune_cache_clear", "tune_cache_size", "dist_rows", "Comm", "status_string", "EXPORTED_SYMBOLS",
 ]
 
 ALGO_AUTO, ALGO_TF32X3, ALGO_SIMT_F32, ALGO_TF32X1 = 0, 1, 2, 3
@@ -28,6 +29,8 @@ EXPORTED_SYMBOLS = [
     "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_op", "tm_sgemm_colmajor", "tm_conv2d_nhwc", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
     "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
     "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
+    "tm_sgemm_tune", "tm_tune_cache_size", "tm_tune_cache_clear", "tm_tune_cache_save", "tm_tune_cache_load",
+    "tm_sgemm_plan_config",
 ]
 
 
@@ -66,6 +69,13 @@ def _load():
     L.tm_sgemm_dist.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, i64, ci, f32, vp, i64, vp]
     L.tm_sgemm_dist_loopback.argtypes = [ci, ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, vp]
     L.tm_sgemm_dist_allgather.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, vp, i64, f32, vp, i64, vp]
+    pi = ctypes.POINTER(ci)
+    L.tm_sgemm_tune.argtypes = [ci, ci] + gemm + [ci, pi, pi, pi, ctypes.POINTER(f32)]
+    L.tm_tune_cache_size.argtypes = []
+    L.tm_tune_cache_clear.argtypes = []
+    L.tm_tune_cache_save.argtypes = [ctypes.c_char_p]
+    L.tm_tune_cache_load.argtypes = [ctypes.c_char_p]
+    L.tm_sgemm_plan_config.argtypes = [ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, ci, pi, pi, pi, pi]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(L, name)
         if fn.restype is ctypes.c_int or name in ("tm_status_string", "tm_sgemm_plan_name"):
@@ -156,6 +166,57 @@ def sgemm_op(A, B, C, alpha: float = 1.0, beta: float = 0.0, opa: str = "N", opb
                          _ptr(C), _ld(C), _stream(stream), int(algo))
     _check(st, "tm_sgemm_op")
     return C
+
+
+def tune(A, B, C, alpha: float = 1.0, beta: float = 0.0, opa: str = "N", opb: str = "N", reps: int = 5,
+         stream=None):
+    """Time every tensor-core configuration on these operands (C is read, not
+    written) and cache the fastest for this shape; later calls use it.
+    Returns (cg, bn_cta, streamk, median_ms)."""
+    A, B, C = _f32("A", A), _f32("B", B), _f32("C", C)
+    m, n = C.shape
+    ta, tb = opa == "T", opb == "T"
+    k = A.shape[0] if ta else A.shape[1]
+    cg, bn, sk, ms = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_float()
+    st = lib.tm_sgemm_tune(int(ta), int(tb), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B), float(beta),
+                           _ptr(C), _ld(C), _stream(stream), int(reps), ctypes.byref(cg), ctypes.byref(bn),
+                           ctypes.byref(sk), ctypes.byref(ms))
+    _check(st, "tm_sgemm_tune")
+    return cg.value, bn.value, sk.value, ms.value
+
+
+def plan_config(m, n, k, alpha=1.0, beta=0.0, A_ptr=1 << 12, lda=None, B_ptr=1 << 16, ldb=None, C_ptr=1 << 24,
+                ldc=None, opa="N", opb="N", algo=ALGO_AUTO):
+    """Host-only: (path, cg, bn_cta, streamk) tm_sgemm_op would use; path 3 =
+    tensor cores, 4 = SIMT, 2 = scale, 1 = no-op, 0 = invalid."""
+    ta, tb = opa == "T", opb == "T"
+    lda = (max(m, 1) if ta else max(k, 1)) if lda is None else lda
+    ldb = (max(k, 1) if tb else max(n, 1)) if ldb is None else ldb
+    ldc = max(n, 1) if ldc is None else ldc
+    out = [ctypes.c_int() for _ in range(4)]
+    lib.tm_sgemm_plan_config(int(ta), int(tb), m, n, k, float(alpha), ctypes.c_void_p(A_ptr), lda,
+                             ctypes.c_void_p(B_ptr), ldb, float(beta), ctypes.c_void_p(C_ptr), ldc, int(algo),
+                             *[ctypes.byref(o) for o in out])
+    return tuple(o.value for o in out)
+
+
+def tune_cache_save(path: str) -> None:
+    _check(lib.tm_tune_cache_save(path.encode()), "tm_tune_cache_save")
+
+
+def tune_cache_load(path: str) -> int:
+    n = lib.tm_tune_cache_load(path.encode())
+    if n < 0:
+        raise OSError(f"cannot read {path}")
+    return n
+
+
+def tune_cache_clear() -> None:
+    _check(lib.tm_tune_cache_clear(), "tm_tune_cache_clear")
+
+
+def tune_cache_size() -> int:
+    return lib.tm_tune_cache_size()
 
 
 def conv2d_nhwc(X, Wt, Y, alpha: float = 1.0, beta: float = 0.0, pad: int = 0, algo: int = ALGO_AUTO, stream=None):

@@ -115,6 +115,12 @@ Plan make_plan(const GemmArgs& a, int algo, int num_sms) {
   if (pl.path == Path::kTc) {
     pl.tc = plan_tc(a.m, a.n, a.k, num_sms > 0 ? num_sms : 148);
     pl.tc.split3 = (algo != TM_ALGO_TF32X1);
+    TcChoice tuned;
+    if (pl.tc.split3 && tune_lookup(a, num_sms > 0 ? num_sms : 148, &tuned)) {  // measured choice (tune.cpp)
+      pl.tc.cg = tuned.cg;
+      pl.tc.bn_cta = tuned.bn_cta;
+      pl.tc.streamk = tuned.streamk;
+    }
     const char* force = std::getenv("TM_TC_CONFIG");  // "cg,bn[,sk]" -- tests/bench only
     if (force) {
       int cg = 0, bn = 0, sk = -1;
@@ -215,6 +221,8 @@ std::mutex g_sk_mu;
 std::map<std::pair<int, cudaStream_t>, SkWorkspace> g_sk;
 
 }  // namespace
+
+bool tc_plan_ok(const GemmArgs& a) { return make_plan(a, TM_ALGO_TF32X3, 148).path == Path::kTc; }
 
 tm_status sgemm_reserve(const GemmArgs& a, cudaStream_t stream, int sm_reserve) {
   try {
@@ -365,6 +373,26 @@ tm_status tm_sgemm_colmajor(char transa, char transb, int64_t m, int64_t n, int6
   const int ta = op(transa), tb = op(transb);
   if (ta < 0 || tb < 0) return TM_ERR_INVALID_VALUE;
   return tm_sgemm_op(tb, ta, n, m, k, alpha, B, ldb, A, lda, beta, C, ldc, stream, TM_ALGO_AUTO);
+}
+
+tm_status tm_sgemm_plan_config(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha, const float* A,
+                               int64_t lda, const float* B, int64_t ldb, float beta, const float* C, int64_t ldc,
+                               int algo, int* path, int* cg, int* bn_cta, int* streamk) {
+  if ((opa != TM_OP_N && opa != TM_OP_T) || (opb != TM_OP_N && opb != TM_OP_T)) return TM_ERR_INVALID_VALUE;
+  GemmArgs a{m, n, k, alpha, beta, A, lda, B, ldb, const_cast<float*>(C), ldc, opa == TM_OP_T, opb == TM_OP_T};
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
+  }
+  cudaGetLastError();  // no device (CPU host): plan for 148 SMs
+  tmk::Plan pl = tmk::make_plan(a, algo, sms);
+  if (path) *path = static_cast<int>(pl.path);
+  if (cg) *cg = pl.path == tmk::Path::kTc ? pl.tc.cg : 0;
+  if (bn_cta) *bn_cta = pl.path == tmk::Path::kTc ? pl.tc.bn_cta : 0;
+  if (streamk) *streamk = pl.path == tmk::Path::kTc && pl.tc.streamk ? 1 : 0;
+  return pl.path == tmk::Path::kInvalid ? TM_ERR_INVALID_VALUE : TM_OK;
 }
 
 const char* tm_sgemm_plan_name(int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda,

@@ -41,6 +41,8 @@ inline tm_status launch_tc(const GemmArgs& a, const TcChoice& c, int num_sms, cu
 }
 tm_status launch_simt(const GemmArgs& a, cudaStream_t stream);
 tm_status launch_scale(int64_t m, int64_t n, float beta, float* C, int64_t ldc, cudaStream_t stream);
+// Reads `bytes` (a multiple of 16) of `buf` to evict L2 between timed runs (tune.cpp).
+tm_status launch_l2_flush(const float* buf, int64_t bytes, cudaStream_t stream);
 
 // tm_sgemm with `sm_reserve` SMs left free (distributed mode, so the NCCL
 // broadcast kernels can run concurrently with the persistent GEMM).
@@ -76,6 +78,12 @@ tm_status launch_conv_simt(const ConvArgs& a, cudaStream_t stream);
 // filters that fit in shared memory (tc_conv_direct.cu).
 bool conv_direct_fits(const ConvArgs& a);
 tm_status launch_conv_direct(const ConvArgs& a, int num_sms, cudaStream_t stream);
+
+// Measured-configuration cache (tune.cpp): the tuned choice for this problem
+// shape on `sms` SMs, if tm_sgemm_tune (or tm_tune_cache_load) recorded one.
+bool tune_lookup(const GemmArgs& a, int sms, TcChoice* out);
+// Whether tm_sgemm_op(..., TM_ALGO_TF32X3) would accept these arguments (host-only).
+bool tc_plan_ok(const GemmArgs& a);
 
 // Picks the tensor-core configuration for a shape (planner, plan.cpp).
 TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms);

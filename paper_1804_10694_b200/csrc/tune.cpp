@@ -1,0 +1,202 @@
+// tune.cpp -- measured configuration choice for the tensor-core GEMM
+// (the paper auto-tuned its sgemm's tile sizes,
+// PAPER.md:831-832).
+//
+// tm_sgemm_tune times every compiled tensor-core configuration -- CTA group
+// (1 or 2 SMs), CTA tile width (32, 64, 128 columns), data-parallel or
+// stream-K schedule -- on the caller's operands, writing into a scratch copy
+// of C, with L2 evicted before each run and the candidates interleaved, and
+// records the fastest (median) in a process-wide cache keyed by the problem
+// shape.  The AUTO planner (api.cpp make_plan) consults the cache before its
+// cost model.  The cache can be saved to / loaded from a text file, one entry
+// per line:  m n k ta tb beta_nonzero sms cg bn_cta streamk
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "tm.h"
+#include "tm_internal.h"
+
+namespace tmk {
+namespace {
+
+using Key = std::tuple<int64_t, int64_t, int64_t, int, int, int, int>;  // m n k ta tb beta!=0 sms
+
+std::mutex g_mu;
+std::map<Key, TcChoice>& cache() {
+  static std::map<Key, TcChoice> c;
+  return c;
+}
+
+Key key_of(const GemmArgs& a, int sms) {
+  return Key{a.m, a.n, a.k, a.ta ? 1 : 0, a.tb ? 1 : 0, a.beta != 0.0f ? 1 : 0, sms};
+}
+
+bool valid_choice(int cg, int bn, int sk) {
+  return (cg == 1 || cg == 2) && (bn == 32 || bn == 64 || bn == 128) && (sk == 0 || sk == 1);
+}
+
+}  // namespace
+
+bool tune_lookup(const GemmArgs& a, int sms, TcChoice* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = cache().find(key_of(a, sms));
+  if (it == cache().end()) return false;
+  *out = it->second;
+  return true;
+}
+
+}  // namespace tmk
+
+using tmk::GemmArgs;
+using tmk::TcChoice;
+
+extern "C" {
+
+tm_status tm_sgemm_tune(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda,
+                        const float* B, int64_t ldb, float beta, const float* C, int64_t ldc, void* stream, int reps,
+                        int* best_cg, int* best_bn, int* best_sk, float* best_ms) {
+  if ((opa != TM_OP_N && opa != TM_OP_T) || (opb != TM_OP_N && opb != TM_OP_T)) return TM_ERR_INVALID_VALUE;
+  if (reps < 1 || reps > 1000) return TM_ERR_INVALID_VALUE;
+  if (m <= 0 || n <= 0 || k <= 0 || alpha == 0.0f) return TM_ERR_INVALID_VALUE;  // nothing to tune
+  {
+    GemmArgs v{m, n, k, alpha, beta, A, lda, B, ldb, const_cast<float*>(C), ldc, opa == TM_OP_T, opb == TM_OP_T};
+    if (!tmk::tc_plan_ok(v)) return TM_ERR_INVALID_VALUE;  // same argument rules as tm_sgemm_op(TF32X3)
+  }
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TM_ERR_UNSUPPORTED_DEVICE;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return TM_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // scratch C: the trials write here, the caller's C is only read (beta != 0)
+  const int64_t cbytes = ((m - 1) * ldc + n) * static_cast<int64_t>(sizeof(float));
+  float* scratch = nullptr;
+  if (cudaMalloc(&scratch, static_cast<size_t>(cbytes)) != cudaSuccess) return TM_ERR_CUDA;
+  GemmArgs a{m, n, k, alpha, beta, A, lda, B, ldb, scratch, ldc, opa == TM_OP_T, opb == TM_OP_T};
+  // L2 eviction buffer (2x L2, read between timed runs: the timings then
+  // match a cold-operand call and bench.py's flushed measurement)
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  const int64_t fbytes = std::max<int64_t>(2LL * l2, 64LL << 20) & ~int64_t(15);
+  float* fbuf = nullptr;
+  if (cudaMalloc(&fbuf, static_cast<size_t>(fbytes)) != cudaSuccess) {
+    cudaFree(scratch);
+    return TM_ERR_CUDA;
+  }
+  cudaMemsetAsync(fbuf, 0, static_cast<size_t>(fbytes), s);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  TcChoice choice{0, 0, true, false};
+  tm_status st = TM_OK;
+  std::vector<TcChoice> cands;
+  for (int cg : {2, 1})
+    for (int bn : {128, 64, 32})
+      for (int sk : {0, 1}) cands.push_back(TcChoice{cg, bn, true, sk == 1});
+  std::vector<std::vector<float>> times(cands.size());
+  std::vector<bool> ok(cands.size(), true);
+  // rounds interleave the candidates (clock / power drift hits all alike);
+  // round 0 is a warm-up (first-use setup of each configuration)
+  for (int r = 0; r <= reps && st == TM_OK; ++r) {
+    for (size_t ci = 0; ci < cands.size() && st == TM_OK; ++ci) {
+      if (!ok[ci]) continue;
+      if (beta != 0.0f &&
+          cudaMemcpyAsync(scratch, C, static_cast<size_t>(cbytes), cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+        st = TM_ERR_CUDA;
+        break;
+      }
+      tmk::launch_l2_flush(fbuf, fbytes, s);
+      cudaEventRecord(e0, s);
+      const bool launched = tmk::launch_tc(a, cands[ci], sms, s) == TM_OK;
+      cudaEventRecord(e1, s);
+      if (!launched || cudaEventSynchronize(e1) != cudaSuccess) {
+        ok[ci] = false;
+        if (cudaGetLastError() != cudaSuccess) st = TM_ERR_CUDA;  // sticky error: stop
+        continue;
+      }
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r > 0) times[ci].push_back(ms);
+    }
+  }
+  for (size_t ci = 0; ci < cands.size() && st == TM_OK; ++ci) {
+    if (!ok[ci] || times[ci].empty()) continue;
+    auto& t = times[ci];
+    std::nth_element(t.begin(), t.begin() + t.size() / 2, t.end());
+    const float med = t[t.size() / 2];
+    if (med < best) {
+      best = med;
+      choice = cands[ci];
+    }
+  }
+  cudaFree(fbuf);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(scratch);
+  if (st != TM_OK) return st;
+  if (choice.cg == 0) return TM_ERR_CUDA;
+  {
+    std::lock_guard<std::mutex> lk(tmk::g_mu);
+    tmk::cache()[tmk::key_of(a, sms)] = choice;
+  }
+  if (best_cg) *best_cg = choice.cg;
+  if (best_bn) *best_bn = choice.bn_cta;
+  if (best_sk) *best_sk = choice.streamk ? 1 : 0;
+  if (best_ms) *best_ms = best;
+  return TM_OK;
+}
+
+int tm_tune_cache_size(void) {
+  std::lock_guard<std::mutex> lk(tmk::g_mu);
+  return static_cast<int>(tmk::cache().size());
+}
+
+tm_status tm_tune_cache_clear(void) {
+  std::lock_guard<std::mutex> lk(tmk::g_mu);
+  tmk::cache().clear();
+  return TM_OK;
+}
+
+tm_status tm_tune_cache_save(const char* path) {
+  if (!path) return TM_ERR_INVALID_VALUE;
+  std::lock_guard<std::mutex> lk(tmk::g_mu);
+  FILE* f = std::fopen(path, "w");
+  if (!f) return TM_ERR_INVALID_VALUE;
+  std::fprintf(f, "# tm tune cache: m n k ta tb beta_nonzero sms cg bn_cta streamk\n");
+  for (const auto& [key, c] : tmk::cache()) {
+    const auto& [m, n, k, ta, tb, bnz, sms] = key;
+    std::fprintf(f, "%lld %lld %lld %d %d %d %d %d %d %d\n", static_cast<long long>(m), static_cast<long long>(n),
+                 static_cast<long long>(k), ta, tb, bnz, sms, c.cg, c.bn_cta, c.streamk ? 1 : 0);
+  }
+  return std::fclose(f) == 0 ? TM_OK : TM_ERR_INVALID_VALUE;
+}
+
+int tm_tune_cache_load(const char* path) {
+  if (!path) return -1;
+  FILE* f = std::fopen(path, "r");
+  if (!f) return -1;
+  int loaded = 0;
+  char line[256];
+  std::lock_guard<std::mutex> lk(tmk::g_mu);
+  while (std::fgets(line, sizeof line, f)) {
+    if (line[0] == '#') continue;
+    long long m, n, k;
+    int ta, tb, bnz, sms, cg, bn, sk;
+    if (std::sscanf(line, "%lld %lld %lld %d %d %d %d %d %d %d", &m, &n, &k, &ta, &tb, &bnz, &sms, &cg, &bn, &sk) != 10)
+      continue;
+    if (m <= 0 || n <= 0 || k <= 0 || (ta | tb | bnz) > 1 || ta < 0 || tb < 0 || bnz < 0 || sms <= 0 ||
+        !tmk::valid_choice(cg, bn, sk))
+      continue;  // malformed entries are skipped
+    tmk::cache()[tmk::Key{m, n, k, ta, tb, bnz, sms}] = TcChoice{cg, bn, true, sk == 1};
+    ++loaded;
+  }
+  std::fclose(f);
+  return loaded;
+}
+
+}  // extern "C"
