@@ -121,7 +121,7 @@ tm_status tm_sgemm_colmajor(char transa, char transb, int64_t m, int64_t n, int6
  *   Y[b,y,x,f] = alpha * sum_{ky,kx,c} X[b, y+ky-pad, x+kx-pad, c] * Wt[f,ky,kx,c] + beta * Y[b,y,x,f]
  * (X outside the image reads as zero).  AUTO uses a 3xTF32 tensor-core path
  * when c % 16 == 0, f % 4 == 0, pointers 16-byte aligned and pad <= 127 --
- * the direct halo-tile kernel when s is 1 or 3, r * c <= 128 and f <= 64
+ * the direct halo-tile kernel when s is 1, 3, 5 or 7, r * c <= 128 and f <= 64
  * (filters resident in shared memory), else the implicit-GEMM kernel (A =
  * im2col of X streamed by TMA im2col-mode copies, never materialised) -- and
  * otherwise the FP32 SIMT direct convolution; TM_ALGO_TF32X3 on shapes

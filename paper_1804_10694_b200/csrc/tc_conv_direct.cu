@@ -363,7 +363,7 @@ bool encode_filters(CUtensorMap* map, const ConvArgs& a, int fp) {
 // Fills p and returns the dynamic shared-memory size, or 0 if the shape does
 // not fit the direct kernel (then the implicit-GEMM kernel runs).
 int dc_plan(const ConvArgs& a, DcParams& p) {
-  if (a.s != 1 && a.s != 3) return 0;
+  if (a.s != 1 && a.s != 3 && a.s != 5 && a.s != 7) return 0;
   if (a.c % kDcBK != 0 || a.r * a.c > 128 || a.f > 64 || a.r > 8) return 0;
   const int64_t ho = a.ho(), wo = a.wo();
   if (ho <= 0 || wo <= 0) return 0;
@@ -443,7 +443,12 @@ tm_status launch_conv_direct(const ConvArgs& a, int num_sms, cudaStream_t stream
   DcParams p;
   const int smem = dc_plan(a, p);
   if (smem == 0) return TM_ERR_INVALID_VALUE;
-  return a.s == 3 ? launch_dc<3>(a, p, smem, num_sms, stream) : launch_dc<1>(a, p, smem, num_sms, stream);
+  switch (a.s) {
+    case 1: return launch_dc<1>(a, p, smem, num_sms, stream);
+    case 3: return launch_dc<3>(a, p, smem, num_sms, stream);
+    case 5: return launch_dc<5>(a, p, smem, num_sms, stream);
+    default: return launch_dc<7>(a, p, smem, num_sms, stream);
+  }
 }
 
 }  // namespace tmk

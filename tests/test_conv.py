@@ -70,7 +70,7 @@ def test_conv_tensor_core_configs(config, shape):
 DIRECT_SHAPES = [(2, 6, 300, 16, 16, 3, 3, 1), (3, 5, 128, 16, 16, 3, 3, 1), (1, 4, 257, 32, 32, 3, 3, 1),
                  (2, 5, 140, 48, 20, 3, 3, 1), (1, 4, 130, 64, 64, 3, 3, 1), (2, 7, 150, 16, 8, 5, 5, 2),
                  (2, 6, 131, 16, 40, 1, 1, 0), (1, 9, 200, 32, 16, 3, 5, 0), (2, 3, 1, 16, 16, 3, 3, 1),
-                 (1, 40, 3, 16, 12, 3, 1, 1)]
+                 (1, 40, 3, 16, 12, 3, 1, 1), (1, 9, 140, 16, 16, 3, 7, 3), (2, 6, 133, 16, 24, 5, 5, 2)]
 
 
 @pytest.mark.parametrize("shape", DIRECT_SHAPES)
