@@ -234,7 +234,7 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 // right edge, and rows past m, are predicated element by element -- nothing
 // outside m x n is read or written.  beta == 0 never reads C.
 template <int KCOLS>
-__device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, int m, int n, int row0, int col0,
+__device__ __forceinline__ void epi_store_lowreg(float* __restrict__ C, long long ldc, int m, int n, int row0, int col0,
                                           const float (&acc)[KCOLS], float alpha, float beta, float* stage,
                                           int lane) {
   constexpr int SWD = KCOLS < 16 ? KCOLS : 16;  // slab width (columns)
@@ -293,6 +293,92 @@ __device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, 
       }
     }
     __syncwarp();
+  }
+}
+
+template <int KCOLS>
+__device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, int m, int n, int row0, int col0,
+                                          const float (&acc)[KCOLS], float alpha, float beta, float* stage,
+                                          int lane) {
+  constexpr int SWD = KCOLS < 16 ? KCOLS : 16;  // slab width (columns)
+  constexpr int G = SWD / 4;                     // 16-byte groups per slab row
+  constexpr int RPI = 32 / G;                    // rows covered by one warp-wide access
+  constexpr int NI = 32 / RPI;                   // accesses per slab
+  constexpr int NSLAB = KCOLS / SWD;
+  // beta*C loads issued together: the epilogue is bound by the C-load round
+  // trip (L2 or DRAM), so for KCOLS <= 64 all of a warp's loads go out at once
+  // (SB slabs x RB row groups = KCOLS extra registers); KCOLS 128, whose 128
+  // accumulator registers leave no room, keeps two loads in flight per slab.
+  if constexpr (NSLAB > 4) {
+    epi_store_lowreg<KCOLS>(C, ldc, m, n, row0, col0, acc, alpha, beta, stage, lane);
+    return;
+  }
+  constexpr int SB = NSLAB <= 4 ? NSLAB : 1;
+  constexpr int RB = NSLAB <= 4 ? NI : 2;
+  const int cc = (lane % G) * 4;
+#pragma unroll
+  for (int c0 = 0; c0 < NSLAB; c0 += SB) {
+#pragma unroll
+    for (int i0 = 0; i0 < NI; i0 += RB) {
+      float4 cv[SB][RB];
+#pragma unroll
+      for (int sb = 0; sb < SB; ++sb) {
+        const int col = col0 + (c0 + sb) * SWD + cc;
+        const bool full_cols = col + 3 < n;
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          cv[sb][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          const int row = row0 + (i0 + i) * RPI + lane / G;
+          if (beta != 0.0f && row < m) {
+            const float* cp = C + static_cast<long long>(row) * ldc + col;
+            if (full_cols) {
+              cv[sb][i] = *reinterpret_cast<const float4*>(cp);
+            } else {
+              if (col < n) cv[sb][i].x = cp[0];
+              if (col + 1 < n) cv[sb][i].y = cp[1];
+              if (col + 2 < n) cv[sb][i].z = cp[2];
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int sb = 0; sb < SB; ++sb) {
+        const int c = (c0 + sb) * SWD;
+        if (i0 == 0) {  // stage this slab (lane = row) for row-group reads
+#pragma unroll
+          for (int j = 0; j < SWD; j += 4)
+            *reinterpret_cast<float4*>(stage + lane * kEpiStride + j) =
+                make_float4(acc[c + j], acc[c + j + 1], acc[c + j + 2], acc[c + j + 3]);
+          __syncwarp();
+        }
+        const int col = col0 + c + cc;
+        const bool full_cols = col + 3 < n;
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          const int r = (i0 + i) * RPI + lane / G;
+          const int row = row0 + r;
+          const float4 v = *reinterpret_cast<const float4*>(stage + r * kEpiStride + cc);
+          if (row >= m) continue;
+          float4 o;
+          if (beta == 0.0f) {
+            o = make_float4(alpha * v.x, alpha * v.y, alpha * v.z, alpha * v.w);
+          } else {
+            const float4 q = cv[sb][i];
+            o = make_float4(fmaf(alpha, v.x, beta * q.x), fmaf(alpha, v.y, beta * q.y),
+                            fmaf(alpha, v.z, beta * q.z), fmaf(alpha, v.w, beta * q.w));
+          }
+          float* cp = C + static_cast<long long>(row) * ldc + col;
+          if (full_cols) {
+            *reinterpret_cast<float4*>(cp) = o;
+          } else {
+            if (col < n) cp[0] = o.x;
+            if (col + 1 < n) cp[1] = o.y;
+            if (col + 2 < n) cp[2] = o.z;
+          }
+        }
+        if (i0 + RB == NI) __syncwarp();  // slab done: the stage may be rewritten
+      }
+    }
   }
 }
 
@@ -366,7 +452,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) ptx::tmem_alloc<CG>(tmem_base_slot, kTmemCols);
   ptx::tc_fence_before();
   __syncthreads();
-  if constexpr (CG == 2) ptx::cluster_sync();
+  // The TMA producers touch only this CTA's shared memory and barriers, so they
+  // start loading before the cluster barrier completes (they wait for it after
+  // their loop); every other role needs the peer CTA initialised.
+  if constexpr (CG == 2) ptx::cluster_arrive();  // each role waits below
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   if (threadIdx.x == 0) trace_mark(p, 1);
@@ -402,8 +491,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int rows_here = min(kBMCta, p.m - row0);
           for (int kb = u.kb0; kb < u.kb1; ++kb) {
             if (own == pi) {
-              if (kb == max(u.kb0, u.kb1 - p.kc_blocks) && u.kb1 == p.kblocks && p.beta != 0.0f && rows_here > 0) {
-                // This unit's epilogue will read beta*C: stage this CTA's C rows
+              if (kb == max(u.kb0, u.kb1 - p.kc_blocks) && u.kb0 == 0 && p.beta != 0.0f && rows_here > 0) {
+                // This unit ends in the epilogue (a whole tile or a stream-K
+                // finalizer) and will read beta*C: stage this CTA's C rows
                 // in L2 about one K_c chunk (plus the ring depth) ahead, so the
                 // epilogue's loads hit L2 instead of exposing DRAM latency.
                 const int c0 = tni * Cfg::kTileN;
@@ -448,8 +538,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (pi == 0) trace_mark(p, 2);  // producer done issuing
       }
+      __syncwarp();
+      if constexpr (CG == 2) ptx::cluster_wait();  // the barrier phase this warp arrived at on entry
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
+      if constexpr (CG == 2) ptx::cluster_wait();
+      ptx::tc_fence_after();
       if (rank == 0 && ptx::elect_one()) {
         constexpr uint32_t idesc = ptx::idesc_tf32(Cfg::kMmaM, Cfg::kMmaN, /*A MN-major*/ TA ? 1 : 0,
                                                    /*B MN-major*/ TB ? 0 : 1);
@@ -467,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t loA_s = ptx::smem_u32(loA), loB_s = ptx::smem_u32(loB);
         int s = 0, sl = 0, pb = 0;
         uint32_t ph = 0, phl = 0, pph = 0;
+        bool first_mma = p.trace != nullptr;
         UnitIter ui = units_begin(p, cluster_id, num_clusters);
         Unit u;
         while (units_next(p, num_clusters, ui, u)) {
@@ -478,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kb = kb0; kb < kb1; ++kb) {
               ptx::mbar_wait_cluster(&ready[sl], phl);
               ptx::tc_fence_after();
-              if (kb == 0 && s == 0 && ph == 0) trace_mark(p, 4);  // first MMA issue
+              if (first_mma) { trace_mark(p, 4); first_mma = false; }  // first MMA issue
 #pragma unroll
               for (int ks = 0; ks < BK / 8; ++ks) {
                 const uint64_t aH = TA ? desc_mn(rawA_s + s * Cfg::kABytes, ks) : desc_k(rawA_s + s * Cfg::kABytes, ks);
@@ -516,6 +611,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < 8) {
     // ------------------------------------------------------------ split
     ptx::setmaxnreg_dec<64>();  // split warpgroup: (80 + 64) * 128 + 184 * 256 = 65536
+    if constexpr (CG == 2) ptx::cluster_wait();
+    ptx::tc_fence_after();
     const int st = threadIdx.x - 128;
     const uint32_t rawA_s = ptx::smem_u32(rawA), rawB_s = ptx::smem_u32(rawB);
     const uint32_t loA_s = ptx::smem_u32(loA), loB_s = ptx::smem_u32(loB);
@@ -570,6 +667,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ------------------------------------------------------------ promotion + epilogue
     ptx::setmaxnreg_inc<184>();
+    if constexpr (CG == 2) ptx::cluster_wait();
+    ptx::tc_fence_after();
     const int q = warp & 3;             // TMEM lane quarter (rows 32q..32q+31 of this CTA)
     const int h = (warp - 8) >> 2;      // column half
     int pb = 0;
@@ -612,6 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (++pb == 2) { pb = 0; pph ^= 1; }
       }
+      if (warp == 8 && lane == 0) trace_mark(p, 3);  // last TMEM partial of this unit drained
       // Workspace slice of this warp in a cluster's partial: [rank][warp][KCOLS/4][32 lanes] float4,
       // so every warp-wide access is 512 contiguous bytes; the same warp/lane of
       // every cluster uses the same offsets, so partials line up element by element.

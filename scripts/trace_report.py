@@ -5,7 +5,7 @@ import sys
 
 import numpy as np
 
-NAMES = ["entry", "setup_done", "producer_done", "first_stage_landed", "first_mma", "last_mma_issued",
+NAMES = ["entry", "setup_done", "producer_done", "partials_drained(last unit)", "first_mma", "last_mma_issued",
          "acc_done(last unit)", "epilogue_done(last unit)"]
 for line in open(sys.argv[1]):
     d = json.loads(line)
