@@ -241,6 +241,24 @@ tm_status tm_dist_chunk(int64_t k, int nranks, int idx, int64_t* k0, int64_t* kr
 
 namespace {
 
+// Whether the GEMM of chunk c is expected to run while later chunks are still
+// being transferred, i.e. needs SMs left free for the broadcast kernels.  Model:
+// chunk c's GEMM starts when chunk 0 has arrived plus c chunk-GEMM times;
+// the broadcast ends after all chunks at the link rate.  Chunk GEMMs past that
+// point get every SM (the 16 reserved SMs are ~11% of the machine).  If the
+// estimate is optimistic the only cost is a broadcast kernel waiting for SMs
+// (no GEMM ever waits inside a kernel on the broadcast).  Rates: NVLink ~700
+// GB/s per rank, 3xTF32 GEMM ~240 TFLOP/s (measured C5; TM_DIST_LINK_GBS and
+// TM_DIST_GEMM_TFLOPS override them).
+bool chunk_overlaps_transfer(int c, int nchunks, int64_t rows, int64_t n, int64_t kc, int64_t ldb) {
+  static const double link = [] { const char* e = std::getenv("TM_DIST_LINK_GBS"); return e ? std::atof(e) : 700.0; }();
+  static const double gemm = [] { const char* e = std::getenv("TM_DIST_GEMM_TFLOPS"); return e ? std::atof(e) : 240.0; }();
+  if (link <= 0.0 || gemm <= 0.0) return true;
+  const double t_xfer = 4.0 * static_cast<double>(kc) * static_cast<double>(ldb) / (link * 1e9);  // one chunk
+  const double t_gemm = 2.0 * static_cast<double>(rows) * static_cast<double>(n) * static_cast<double>(kc) / (gemm * 1e12);
+  return t_xfer + c * t_gemm < nchunks * t_xfer;
+}
+
 // The per-rank schedule of the row-sharded GEMM, shared by the NCCL mode and
 // the single-process loopback mode.  `xfer(p, count)` enqueues the transfer of
 // `count` floats of B at `p` from the root on `comm_stream` (ncclBroadcast, or
@@ -283,7 +301,8 @@ tm_status dist_schedule(int nranks, int rank, int root, int64_t m, int64_t n, in
     if (cudaStreamWaitEvent(stream, ev_chunk[used], 0) != cudaSuccess) return TM_ERR_CUDA;
     if (rows > 0) {
       tmk::GemmArgs ga{rows, n, kr, alpha, k0 == 0 ? beta : 1.0f, A_local + k0, lda, B + k0 * ldb, ldb, C_local, ldc};
-      tm_status st = tmk::sgemm_reserve(ga, stream, comm_ctas());
+      const int reserve = chunk_overlaps_transfer(used, static_cast<int>(nchunks), rows, n, kc, ldb) ? comm_ctas() : 0;
+      tm_status st = tmk::sgemm_reserve(ga, stream, reserve);
       if (st != TM_OK) return st;
     }
   }
@@ -321,12 +340,12 @@ tm_status allgather_schedule(int nranks, int rank, int64_t m, int64_t n, int64_t
   if (cudaStreamWaitEvent(stream, ev_done, 0) != cudaSuccess) return TM_ERR_CUDA;
   if (k0 > 0) {
     tmk::GemmArgs lo{rows, n, k0, alpha, 1.0f, A_local, lda, B_full, ldb, C_local, ldc};
-    st = tmk::sgemm_reserve(lo, stream, reserve);
+    st = tmk::sgemm_reserve(lo, stream, 0);  // the gather is complete: every SM
     if (st != TM_OK) return st;
   }
   if (k0 + kr < k) {
     tmk::GemmArgs hi{rows, n, k - k0 - kr, alpha, 1.0f, A_local + k0 + kr, lda, B_full + (k0 + kr) * ldb, ldb, C_local, ldc};
-    st = tmk::sgemm_reserve(hi, stream, reserve);
+    st = tmk::sgemm_reserve(hi, stream, 0);
     if (st != TM_OK) return st;
   }
   return TM_OK;
