@@ -29,7 +29,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "sgemm GFLOP/s and % of TF32/FP32 roofline at 1/2/4/8 B200 vs CPU oracle"
-ALGOS = {"auto": 0, "tf32x3": 1, "simt": 2}
+ALGOS = {"auto": 0, "tf32x3": 1, "simt": 2, "tf32x1": 3}
 
 
 def load_peaks():
@@ -68,6 +68,8 @@ def roofline_peak(path, peaks):
     if path == "simt":
         return "alu", 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12, "TFLOP/s", "148 SM x 128 FFMA/clk x 2 x sm_max_mhz"
     tf32 = peaks["bf16_tflops"] * (1.1 / 2.25)
+    if path == "tf32x1":  # one MMA per product: the TF32 dense peak itself
+        return "tensor", tf32, "TFLOP/s", f"{peaks['source']} bf16 {peaks['bf16_tflops']} x 1.1/2.25 (tf32, 1xTF32)"
     return "tensor", tf32 / 3.0, "TFLOP/s", f"{peaks['source']} bf16 {peaks['bf16_tflops']} x 1.1/2.25 (tf32) / 3 (3xTF32)"
 
 
@@ -306,7 +308,7 @@ def main():
     value = flops * args.steps / (total_ms * 1e-3) / 1e9  # GFLOP/s, whole job
 
     # roofline of the dominant kernel (the GEMM), from this rank's live event times
-    kernel = "simt" if path == "simt" else "tf32x3"
+    kernel = path if path in ("simt", "tf32x1") else "tf32x3"
     bound, peak, unit, peak_note = roofline_peak(kernel, peaks)
     my_flops = 2.0 * rows * n * k
     my_ms = statistics.mean(per_step)
@@ -331,8 +333,8 @@ def main():
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core, fp32 accumulate)"
-        if kernel != "simt" else "f32", "data": "synthetic (seeded U[-1,1) fp32, device-generated)",
+        "scaling": "strong", "vs_baseline": None, "dtype": {"simt": "f32", "tf32x1": "tf32 (1xTF32 tensor-core, fp32 accumulate)"}.get(
+            kernel, "f32 (3xTF32 tensor-core, fp32 accumulate)"), "data": "synthetic (seeded U[-1,1) fp32, device-generated)",
         "config": {"workload": desc, "m": m, "n": n, "k": k, "alpha": alpha, "beta": beta, "path": path,
                    "rows_per_rank": rows, "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2, no flush" if not small else "L2 flushed (512 MiB read) between steps"},

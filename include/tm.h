@@ -70,8 +70,17 @@ typedef enum {
  *  TM_ALGO_TF32X3    3xTF32 split-operand tcgen05 MMA (fp32 result, TMEM
  *                    accumulation).  Misaligned input -> TM_ERR_INVALID_VALUE.
  *  TM_ALGO_SIMT_F32  pure-FP32 FFMA register-blocked kernel (validation path).
- *  TM_ALGO_TF32X1    single-pass TF32 (about 1e-3 accuracy; does NOT meet the
- *                    1e-5 contract; exposed for data-movement bring-up only). */
+ *  TM_ALGO_TF32X1    single-pass TF32 precision variant:
+ *                    one tcgen05 kind::tf32 MMA per K step on the raw fp32
+ *                    operands, which the tensor core truncates to TF32 (10
+ *                    explicit mantissa bits).  Per product |a_hi b_hi - ab| <=
+ *                    2^-9 |a||b|; with the accumulation of the 3xTF32 path
+ *                    (round-toward-zero partials of K_c = 128, RN promotion)
+ *                    max |C - R| / D <= 2^-9 + 2^-14 for k <= 4096 -- about
+ *                    2e-3; it does NOT meet the 1e-5 contract and AUTO never
+ *                    selects it.  Integer inputs |x| <= 2048 are exact in TF32,
+ *                    so their products are exact.  Same layout rules,
+ *                    transposes and special cases as TF32X3. */
 typedef enum {
     TM_ALGO_AUTO = 0,
     TM_ALGO_TF32X3 = 1,
@@ -97,7 +106,7 @@ tm_status tm_sgemm_ex(int64_t m, int64_t n, int64_t k, float alpha,
  *   opb == TM_OP_N: B is k x n (ldb >= max(1,n)), op(B)[p,j] = B[p*ldb + j]
  *   opb == TM_OP_T: B is n x k (ldb >= max(1,k)), op(B)[p,j] = B[j*ldb + p]
  * C = alpha*op(A)*op(B) + beta*C, C m x n (ldc).  Same paths, accuracy, special
- * cases and errors as tm_sgemm_ex (TM_ALGO_TF32X1 only for N,N). */
+ * cases and errors as tm_sgemm_ex. */
 typedef enum { TM_OP_N = 0, TM_OP_T = 1 } tm_op;
 tm_status tm_sgemm_op(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha,
                       const float* A, int64_t lda, const float* B, int64_t ldb,

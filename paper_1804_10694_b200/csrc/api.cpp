@@ -352,7 +352,6 @@ tm_status tm_conv2d_nhwc(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f,
 tm_status tm_sgemm_op(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha, const float* A, int64_t lda,
                       const float* B, int64_t ldb, float beta, float* C, int64_t ldc, void* stream, int algo) {
   if ((opa != TM_OP_N && opa != TM_OP_T) || (opb != TM_OP_N && opb != TM_OP_T)) return TM_ERR_INVALID_VALUE;
-  if (algo == TM_ALGO_TF32X1 && (opa != TM_OP_N || opb != TM_OP_N)) return TM_ERR_INVALID_VALUE;
   GemmArgs a{m, n, k, alpha, beta, A, lda, B, ldb, C, ldc, opa == TM_OP_T, opb == TM_OP_T};
   try {
     return tmk::run(a, algo, static_cast<cudaStream_t>(stream));

@@ -959,14 +959,13 @@ tm_status launch_split(const GemmArgs& a, int cg, int bn, int num_sms, bool sk, 
 }  // namespace
 
 // Tensor-core launch for one operand layout (explicitly instantiated in
-// tc_gemm_{nn,nt,tn,tt}.cu).  The single-pass TF32 bring-up mode exists only
-// for the NN layout.
+// tc_gemm_{nn,nt,tn,tt}.cu): 3xTF32 (split3) or the single-pass 1xTF32
+// precision variant (one MMA per K step on the raw operands).
 template <bool TA, bool TB>
 tm_status launch_tc_op(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream) {
   if (a.m > INT32_MAX / 2 || a.n > INT32_MAX / 2 || a.k > INT32_MAX / 2) return TM_ERR_INVALID_VALUE;
   if (c.split3) return launch_split<true, TA, TB>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
-  if constexpr (!TA && !TB) return launch_split<false, false, false>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
-  return TM_ERR_INVALID_VALUE;
+  return launch_split<false, TA, TB>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
 }
 
 }  // namespace tmk

@@ -131,6 +131,8 @@ def test_op_and_colmajor_validation_on_host():
     # opb = T: ldb must be >= k
     assert L.tm_sgemm_op(0, 1, 8, 64, 16, 1.0, vp(16), 16, vp(1 << 16), 8, 0.0, vp(1 << 24), 64, None, 0) == 1
     assert L.tm_sgemm_op(2, 0, 8, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None, 0) == 1
-    assert L.tm_sgemm_op(1, 0, 8, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None, 3) == 1
+    # explicit tensor-core paths (3xTF32, 1xTF32) reject a misaligned operand
+    assert L.tm_sgemm_op(1, 0, 8, 8, 8, 1.0, vp(20), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None, 3) == 1
+    assert L.tm_sgemm_op(0, 1, 8, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 10, 0.0, vp(1 << 24), 8, None, 1) == 1
     assert L.tm_sgemm_colmajor(b"X", b"N", 8, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None) == 1
     assert L.tm_sgemm_op(1, 1, 0, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None, 0) == 0  # noop
