@@ -183,6 +183,29 @@ def cpu_oracle_sample(m, n, k, alpha, beta, budget_s=15.0, extra_rows=()):
     return gflops, cores, f"{target} rows x {n} cols x K={k} of the {m}x{n}x{k} workload ({dt:.1f} s)"
 
 
+def parity_sample(tm, torch, A, B, C0, alpha, beta, algo, path):
+    """The timed launch configuration checked against the oracle on sampled
+    rows of THIS run's inputs (part of the cpu_baseline leg): one more call on
+    a fresh copy of C0, then max |C - R| / D over every column of the rows
+    (tile and row-block boundaries plus seeded random rows)."""
+    import numpy as np
+    import oracle
+    m = A.shape[0]
+    Cc = C0.clone()
+    tm.sgemm_ex(A, B, Cc, alpha, beta, algo)
+    torch.cuda.synchronize()
+    rows = {0, 1, m // 2, m - 2, m - 1} | {r for b in range(128, m, 128 * max(1, m // 2048)) for r in (b - 1, b)}
+    rows |= set(np.random.default_rng(7).integers(0, m, size=48).tolist())
+    rows = sorted(r for r in rows if 0 <= r < m)
+    idx = torch.tensor(rows, device=A.device)
+    R, D = oracle.sgemm(alpha, A.index_select(0, idx).cpu().numpy(), B.cpu().numpy(), beta,
+                        C0.index_select(0, idx).cpu().numpy())
+    err = float(np.max(oracle.normalized_error(Cc.index_select(0, idx).cpu().numpy(), R, D)))
+    tol = 2.0 ** -9 + 2.0 ** -14 if path == "tf32x1" else 1e-5
+    return {"rows": len(rows), "cols": int(B.shape[1]), "max_normalized_error": err, "tolerance": tol,
+            "pass": err <= tol}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on the host cores, bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
@@ -273,6 +296,8 @@ def main():
 
     path = tm.plan_name(rows, n, k, alpha, beta, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
                         C.data_ptr(), C.stride(0), algo)
+    check = rank == 0 and not args.no_cpu and world == 1
+    C0 = C.clone() if check else None  # the steps update C in place; the parity sample needs the input
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -349,6 +374,7 @@ def main():
         v, cores, sample = cpu_oracle_sample(m, n, k, alpha, beta, budget_s=15.0)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
                                 "sample": sample}
+        line["cpu_baseline"]["parity_sample"] = parity_sample(tm, torch, A, B, C0, alpha, beta, algo, path)
     if comm is not None:
         comm.close()
     if rank == 0:
