@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               hl[4 * j + e] = x[e];                           // A_hi: kind::tf32 truncates the raw value
               // A_lo = x - hi, exact in fp32, left for the tensor core to truncate
               // (2 ops instead of the RNA rounding's 4: this split warp is the
-              // kernel's critical role; bound 3 * 2^-20 per product, reading 4)
+              // kernel's critical role; bound 5 * 2^-21 per product, reading 4)
               hl[kDcBK + 4 * j + e] = __float_as_uint(__fsub_rn(__uint_as_float(x[e]), __uint_as_float(x[e] & 0xFFFFE000u)));
             }
           }

@@ -1,4 +1,3 @@
-timeout 600 python -m pytest tests/test_conv.py -q -m gpu -p no:cacheprovider -x 2>&1 | tail -3
-bash scripts/ms.sh "conv old" --config CONV --steps 20 --warmup 5 --no-cpu
-TM_DC_ROWBOX=1 bash scripts/ms.sh "conv old rowboxes" --config CONV --steps 20 --warmup 5 --no-cpu
-TM_DC_ROWBOX=1 timeout 600 python -m pytest tests/test_conv.py -q -m gpu -p no:cacheprovider -x 2>&1 | tail -3
+timeout 600 python -m pytest tests/test_conv.py -q -m gpu -p no:cacheprovider -x 2>&1 | tail -2
+for i in 1 2; do bash scripts/ms.sh "conv" --config CONV --steps 20 --warmup 5 --no-cpu; done
+bash scripts/ms.sh "conv beta.5" --config CONV --conv-beta 0.5 --steps 20 --warmup 5 --no-cpu
