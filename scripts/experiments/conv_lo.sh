@@ -1,3 +1,4 @@
+# NOTE: TM_DC_LO_TRUNC was a temporary knob; the truncated A_lo is now the kernel default (reading 4)
 python - <<'PY'
 # accuracy of the paper-shape conv against the oracle on sampled pixels (max normalized error)
 import sys, os; sys.path.insert(0, os.getcwd())
