@@ -89,7 +89,14 @@ typedef enum {
 } tm_algo;
 
 /* C = alpha*A*B + beta*C on `stream`.  A: m x k (lda),
- * B: k x n (ldb), C: m x n (ldc), all row-major fp32 device memory. */
+ * B: k x n (ldb), C: m x n (ldc), all row-major fp32 device memory.
+ * CUDA graphs: the call enqueues only kernels and memsets, so it may be
+ * captured (stream capture) and replayed.  Stream-K schedules use a small
+ * library workspace per (device, stream) that cannot be allocated during
+ * capture: make the same call once on the capturing stream before capturing
+ * (otherwise TM_ERR_INVALID_VALUE); replay on that stream (or serialised with
+ * it).  Workspaces are never freed while the process runs, so captured graphs
+ * stay valid. */
 tm_status tm_sgemm(int64_t m, int64_t n, int64_t k, float alpha,
                    const float* A, int64_t lda, const float* B, int64_t ldb,
                    float beta, float* C, int64_t ldc, void* stream);

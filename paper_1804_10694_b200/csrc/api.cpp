@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <utility>
 
@@ -219,6 +220,9 @@ struct SkWorkspace {
 };
 std::mutex g_sk_mu;
 std::map<std::pair<int, cudaStream_t>, SkWorkspace> g_sk;
+// Workspaces replaced by larger ones are never freed: a CUDA graph captured
+// earlier may still reference them (a few MB each).
+std::vector<void*> g_sk_retired;
 
 }  // namespace
 
@@ -238,8 +242,22 @@ tm_status streamk_workspace(cudaStream_t stream, size_t ws_bytes, size_t flag_co
   if (cudaGetDevice(&dev) != cudaSuccess) return TM_ERR_CUDA;
   std::lock_guard<std::mutex> lk(g_sk_mu);
   SkWorkspace& w = g_sk[{dev, stream}];
+  // CUDA graph capture: no allocation is possible while capturing (run the
+  // same call once outside the capture first), and the graph will be replayed
+  // with the epoch baked into the kernel parameters, so the flags are cleared
+  // inside the graph before every replay and the captured launch uses epoch 1.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) return TM_ERR_CUDA;
+  if (cap == cudaStreamCaptureStatusActive) {
+    if (w.ws_bytes < ws_bytes || w.flag_count < flag_count) return TM_ERR_INVALID_VALUE;
+    if (cudaMemsetAsync(w.flags, 0, w.flag_count * sizeof(unsigned), stream) != cudaSuccess) return TM_ERR_CUDA;
+    *ws = w.ws;
+    *flags = w.flags;
+    *epoch = 1;
+    return TM_OK;
+  }
   if (w.ws_bytes < ws_bytes) {
-    if (w.ws) cudaFree(w.ws);
+    if (w.ws) g_sk_retired.push_back(w.ws);
     w.ws = nullptr;
     w.ws_bytes = 0;
     if (cudaMalloc(&w.ws, ws_bytes) != cudaSuccess) {
@@ -249,7 +267,7 @@ tm_status streamk_workspace(cudaStream_t stream, size_t ws_bytes, size_t flag_co
     w.ws_bytes = ws_bytes;
   }
   if (w.flag_count < flag_count) {
-    if (w.flags) cudaFree(w.flags);
+    if (w.flags) g_sk_retired.push_back(w.flags);
     w.flags = nullptr;
     w.flag_count = 0;
     if (cudaMalloc(&w.flags, flag_count * sizeof(unsigned)) != cudaSuccess) {
@@ -260,7 +278,7 @@ tm_status streamk_workspace(cudaStream_t stream, size_t ws_bytes, size_t flag_co
     w.flag_count = flag_count;
     w.epoch = 0;
   }
-  if (++w.epoch == 0) {  // wrapped: flags could hold any old epoch; clear them
+  if (++w.epoch <= 1) {  // wrapped (or 1, which graph replays use): flags could hold it; clear them
     if (cudaMemsetAsync(w.flags, 0, w.flag_count * sizeof(unsigned), stream) != cudaSuccess) return TM_ERR_CUDA;
     w.epoch = 1;
   }
