@@ -98,40 +98,49 @@ def _check(status: int, what: str):
 
 def _ld(t) -> int:
     """Leading dimension (elements) of a row-major 2-D view with unit column stride."""
-    if t.dim() != 2:
+    sh = t.shape
+    if len(sh) != 2:
         raise ValueError("expected a 2-D tensor")
-    if t.shape[1] > 1 and t.stride(1) != 1:
+    st = t.stride()
+    if sh[1] > 1 and st[1] != 1:
         raise ValueError("expected unit column stride (row-major)")
-    if t.shape[0] <= 1:
-        return max(int(t.stride(0)) if t.shape[0] == 1 else 1, int(t.shape[1]), 1)
-    return int(t.stride(0))
+    if sh[0] <= 1:
+        return max(int(st[0]) if sh[0] == 1 else 1, int(sh[1]), 1)
+    return int(st[0])
 
 
 def _ptr(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    # ctypes converts a Python int (or None) for a c_void_p argument itself
+    return None if t is None else t.data_ptr()
 
 
 _raw_stream = None
 
 
 def _stream(stream):
-    """cudaStream_t of `stream` (int / torch.cuda.Stream) or torch's current stream."""
+    """cudaStream_t (as an int) of `stream` (int / torch.cuda.Stream) or torch's current stream."""
     global _raw_stream
     if stream is not None:
-        return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
-    import torch
+        return int(getattr(stream, "cuda_stream", stream))
     if _raw_stream is None:
+        import torch
         get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
         _raw_stream = (lambda: get(torch.cuda.current_device())) if get else \
             (lambda: torch.cuda.current_stream().cuda_stream)
-    return ctypes.c_void_p(_raw_stream())
+    return _raw_stream()
+
+
+_F32 = None
 
 
 def _f32(name, t):
-    import torch
+    global _F32
     if t is None:
         return None
-    if t.dtype != torch.float32:
+    if _F32 is None:
+        import torch
+        _F32 = torch.float32
+    if t.dtype is not _F32:
         raise TypeError(f"{name} must be float32")
     return t
 
