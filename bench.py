@@ -101,6 +101,15 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.late = False
+        if self.proc and not self.lines:
+            # timed region shorter than nvidia-smi's start-up: take the first
+            # sample just after it (flagged in the summary) rather than none
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0:
+                time.sleep(0.02)
+            self.late = bool(self.lines)
+            del self.lines[1:]
         if self.proc:
             self.proc.terminate()
             try:
@@ -125,7 +134,10 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if getattr(self, "late", False):
+            out["note"] = "timed region shorter than the sampler start-up; one sample taken right after it"
+        return out
 
 
 def workload(name):
