@@ -33,6 +33,8 @@ CFLAGS = ["-O3", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off", "-std=c11"
 
 def build(force: bool = False) -> str:
     """Compile oracle.c into liboracle.so (no-op when up to date)."""
+    if os.environ.get("TM_ORACLE_LIB"):
+        return os.environ["TM_ORACLE_LIB"]
     with _lock:
         stale = (not os.path.exists(_LIB)) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC)
         if force or stale:
@@ -42,11 +44,19 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+def build_mutant(n: int, out: str) -> str:
+    """Compile oracle.c with -DORACLE_MUTANT=n (one step broken on purpose, see
+    oracle.c) into ``out``; used only by tests/test_oracle_mutants.py, which
+    loads it through TM_ORACLE_LIB in a subprocess and expects the pins to fail."""
+    subprocess.check_call(["gcc", *CFLAGS, f"-DORACLE_MUTANT={int(n)}", _SRC, "-o", out, "-lm"])
+    return out
+
+
 def _load():
     global _lib
     if _lib is None:
-        build()
-        lib = ctypes.CDLL(_LIB)
+        path = build()
+        lib = ctypes.CDLL(path)
         i64, f32, vp = ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
         lib.tm_oracle_sgemm_rows.argtypes = [i64, i64, i64, f32, vp, i64, vp, i64,
                                              f32, vp, i64, i64, vp, vp, vp, i64]

@@ -57,6 +57,21 @@
 #include <omp.h>
 #endif
 
+/* Mutation testing of the pins (tests/test_oracle_mutants.py): a build with
+ * -DORACLE_MUTANT=n breaks exactly one step on purpose, and the pin suite must
+ * then fail.  The shipped build is ORACLE_MUTANT == 0, where every MUT(n) is the
+ * constant 0 and the code below is the plain definition.
+ *    1 beta term dropped from R          7 alpha dropped from R
+ *    2 last product (p = k-1) dropped    8 conv: filter taps flipped (convolution vs correlation)
+ *    3 op(B) read transposed             9 conv: padding not subtracted from the input row
+ *    4 lda ignored (A read as dense)    10 dist_rows: the m mod P extra rows go to the LAST ranks
+ *    5 fabs dropped from D              11 beta == 0 still reads C0
+ *    6 beta term subtracted */
+#ifndef ORACLE_MUTANT
+#define ORACLE_MUTANT 0
+#endif
+#define MUT(n) (ORACLE_MUTANT == (n))
+
 static int64_t max1(int64_t x) { return x > 1 ? x : 1; }
 
 static int check_args(int opa, int opb, int64_t m, int64_t n, int64_t k, float alpha,
@@ -87,25 +102,25 @@ static void oracle_row(int opa, int opb, int64_t i, int64_t n, int64_t k, float 
     const double a_beta = (double)beta;
     for (int64_t j = 0; j < n; ++j) { acc[j] = 0.0; acc_abs[j] = 0.0; }
     if (alpha != 0.0f) {
-        for (int64_t p = 0; p < k; ++p) {
-            const double a = (double)(opa ? A[p * lda + i] : A[i * lda + p]);   /* op(A)[i,p] */
-            const double a_abs = fabs(a);
+        for (int64_t p = 0; p < k - MUT(2); ++p) {
+            const double a = (double)(opa ? A[p * lda + i] : A[i * (MUT(4) ? k : lda) + p]);   /* op(A)[i,p] */
+            const double a_abs = MUT(5) ? a : fabs(a);
             for (int64_t j = 0; j < n; ++j) {
-                const double b = (double)(opb ? B[j * ldb + p] : B[p * ldb + j]); /* op(B)[p,j] */
+                const double b = (double)((opb ^ MUT(3)) ? B[j * ldb + p] : B[p * ldb + j]); /* op(B)[p,j] */
                 acc[j] += a * b;             /* exact product, fp64 sum, p ascending */
-                acc_abs[j] += a_abs * fabs(b);
+                acc_abs[j] += a_abs * (MUT(5) ? b : fabs(b));
             }
         }
     }
     for (int64_t j = 0; j < n; ++j) {
         double r = 0.0, d = 0.0;
         if (alpha != 0.0f) {
-            r = a_alpha * acc[j];
+            r = (MUT(7) ? 1.0 : a_alpha) * acc[j];
             d = fabs(a_alpha) * acc_abs[j];
         }
-        if (beta != 0.0f) {               /* beta == 0: C0 is not read */
+        if (beta != 0.0f || (MUT(11) && C0)) {   /* beta == 0: C0 is not read */
             const double c = (double)C0[i * ldc + j];
-            r += a_beta * c;
+            r += (MUT(6) ? -a_beta : MUT(1) ? 0.0 : a_beta) * c;
             d += fabs(a_beta) * fabs(c);
         }
         R_row[j] = r;
@@ -178,6 +193,12 @@ int tm_oracle_sgemm_f64(int64_t m, int64_t n, int64_t k, float alpha,
 int tm_oracle_dist_rows(int64_t m, int nranks, int rank, int64_t *row0, int64_t *rows) {
     if (m < 0 || nranks < 1 || rank < 0 || rank >= nranks || !row0 || !rows) return -1;
     const int64_t q = m / nranks, r = m % nranks;
+    if (MUT(10)) {   /* the plausible slip: remainder rows to the last ranks */
+        const int first_big = nranks - (int)r;
+        *rows = q + (rank >= first_big ? 1 : 0);
+        *row0 = (int64_t)rank * q + (rank > first_big ? rank - first_big : 0);
+        return 0;
+    }
     *rows = q + (rank < r ? 1 : 0);
     *row0 = (int64_t)rank * q + (rank < r ? rank : r);
     return 0;
@@ -237,13 +258,14 @@ int tm_oracle_conv2d_nhwc(int64_t Nb, int64_t H, int64_t W, int64_t C, int64_t F
             double acc = 0.0, acc_abs = 0.0;
             if (alpha != 0.0f) {
                 for (int64_t ky = 0; ky < R; ++ky) {
-                    const int64_t iy = y + ky - pad;
+                    const int64_t iy = y + ky - (MUT(9) ? 0 : pad);
                     for (int64_t kx = 0; kx < S; ++kx) {
                         const int64_t ix = x + kx - pad;
                         for (int64_t c = 0; c < C; ++c) {
                             const double xv = (iy < 0 || iy >= H || ix < 0 || ix >= W)
                                                   ? 0.0 : (double)X[((b * H + iy) * W + ix) * C + c];
-                            const double wv = (double)Wt[((f * R + ky) * S + kx) * C + c];
+                            const int64_t wy = MUT(8) ? R - 1 - ky : ky, wx = MUT(8) ? S - 1 - kx : kx;
+                            const double wv = (double)Wt[((f * R + wy) * S + wx) * C + c];
                             acc += xv * wv;
                             acc_abs += fabs(xv) * fabs(wv);
                         }

@@ -118,7 +118,7 @@ struct TcParams {
   int cv_ho, cv_wo, cv_s, cv_c, cv_pad;
 };
 
-constexpr int kTraceSlots = 8;
+constexpr int kTraceSlots = 16;
 __device__ __forceinline__ void trace_mark(const TcParams& p, int slot) {
   if (p.trace) {
     unsigned long long t;
@@ -620,9 +620,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph = 0, phl = 0;
     UnitIter ui = units_begin(p, cluster_id, num_clusters);
     Unit u;
+    bool first_full = p.trace != nullptr && st == 0;
     while (units_next(p, num_clusters, ui, u)) {
       for (int kb = u.kb0; kb < u.kb1; ++kb) {
         ptx::mbar_wait(&full[s], ph);
+        if (first_full) { trace_mark(p, 8); first_full = false; }  // first TMA stage landed
         // The ready ring must not run more than LO stages ahead of the MMA
         // (an mbarrier phase may not complete twice before it is observed).
         ptx::mbar_wait(&empty_lo[sl], phl ^ 1);
@@ -726,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __threadfence();
         __syncwarp();
         if (lane == 0) st_release_gpu(p.flags + cluster_id * (CG * kEpiWarps) + wslot, p.epoch);
+        if (warp == 8 && lane == 0) trace_mark(p, 9);  // partial published
         continue;
       }
       if (u.kb1 < p.kblocks) {
@@ -740,6 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           const unsigned seen = ld_acquire_gpu(f);  // every lane acquires (orders its own loads below)
           (void)seen;
+          if (warp == 8 && lane == 0) trace_mark(p, 10);  // (last) partial flag acquired
           const float4* w = reinterpret_cast<const float4*>(p.ws) + c2 * ws_stride + ws_off;
           constexpr int kGrp = (KCOLS / 4) < 8 ? (KCOLS / 4) : 8;
 #pragma unroll
@@ -771,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) ptx::cluster_sync();
+  if (threadIdx.x == 0) trace_mark(p, 11);  // teardown barrier passed
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<CG>(tmem_base, kTmemCols);

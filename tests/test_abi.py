@@ -106,6 +106,12 @@ def test_dist_rows_partition():
                 r0, nr = tm.dist_rows(m, P, r)
                 seen.extend(range(r0, r0 + nr))
             assert seen == list(range(m))
+    # the product's partition is the oracle's (pinned by tests/golden/dist_rows.json)
+    import oracle
+    for m in list(range(0, 40)) + [1060, 16383, 16384, 16387]:
+        for P in range(1, 10):
+            for r in range(P):
+                assert tm.dist_rows(m, P, r) == oracle.dist_rows(m, P, r), (m, P, r)
     with pytest.raises(tm.TmError):
         tm.dist_rows(10, 0, 0)
     with pytest.raises(tm.TmError):

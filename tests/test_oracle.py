@@ -226,28 +226,15 @@ def test_normalized_error_metric():
     assert np.isinf(oracle.normalized_error(np.array([[np.nan]], np.float32), R[:, :1], D[:, :1]))[0, 0]
 
 
-def test_pins_catch_mutations():
-    """The pins above are load-bearing: plausible oracle mistakes fail them.
-
-    Each mutation is applied to the oracle's *output* semantics via numpy (we
-    cannot recompile a mutated C file per test cheaply): a transposed operand,
-    a dropped beta term, a sign error, an off-by-one in k.  Each must violate
-    the numpy/brute-force agreement the real oracle satisfies.
-    """
-    m, n, k = 6, 5, 4
-    A, B, C0 = si.matrices(m, n, k, seed=31)
-    A64, B64, C64 = (x.astype(np.float64) for x in (A, B, C0))
-    R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0)
-    good = si.ALPHA * (A64 @ B64) + si.BETA * C64
-    assert np.max(np.abs(R - good) / D) < 1e-12
-    mutants = {
-        "dropped beta": si.ALPHA * (A64 @ B64),
-        "sign": si.ALPHA * (A64 @ B64) - si.BETA * C64,
-        "k off by one": si.ALPHA * (A64[:, :k - 1] @ B64[:k - 1]) + si.BETA * C64,
-        "transposed B": si.ALPHA * (A64 @ B64[::-1, :]) + si.BETA * C64,
-    }
-    for name, mut in mutants.items():
-        assert np.max(np.abs(mut - good) / D) > 1e-3, name
+def test_golden_dist_rows_uneven_partition():
+    """Hand-worked partitions (tests/golden/dist_rows.json, PAPER.md:503-504
+    split(i, N/Ranks), generalised per SURVEY.md 8(b)): the m mod P extra rows
+    go to the first ranks."""
+    with open(os.path.join(GOLDEN, "dist_rows.json")) as f:
+        gold = json.load(f)
+    for case in gold["cases"]:
+        got = [list(oracle.dist_rows(case["m"], case["P"], r)) for r in range(case["P"])]
+        assert got == case["parts"], (case["m"], case["P"], got)
 
 
 @pytest.mark.parametrize("opa,opb", [("N", "T"), ("T", "N"), ("T", "T")])

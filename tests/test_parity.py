@@ -162,7 +162,8 @@ def test_c3b_8192_sampled_rows():
     m, n, k = si.CONFIGS["C3b"]
     A, B, C0 = si.matrices(m, n, k, si.SEEDS["C3b"])
     C, _ = run(A, B, C0, si.ALPHA, si.BETA, AUTO)
-    rows = si.sample_rows(m, count=64, tile=256)
+    rows = si.sample_rows(m, count=2 * m // 128 + 64, tile=128)  # both edge rows of every 128-row band
+    assert len(rows) >= 2 * m // 128
     assert max_err(C, A, B, C0, si.ALPHA, si.BETA, rows=rows) <= TOL
 
 
@@ -179,7 +180,10 @@ def test_large_k_accuracy_sampled_rows(cfg, kind):
     dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C0))
     tm.sgemm(dA, dB, dC, si.ALPHA, si.BETA)
     torch.cuda.synchronize()
-    rows = si.sample_rows(m, count=40, tile=256)
+    # both edge rows of every 128-row band (each CTA's rows of every 256x256
+    # cluster tile) plus 64 seeded random rows -- SURVEY.md 8(d) "every tile row-band"
+    rows = si.sample_rows(m, count=2 * m // 128 + 64, tile=128)
+    assert len(rows) >= 2 * m // 128
     C = dC[torch.from_numpy(rows).cuda()].cpu().numpy()
     del dA, dB, dC
     R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0, rows=rows)
