@@ -83,7 +83,13 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
-        self.lines = []
+        self.lines = []      # (host time of arrival, csv line)
+        self.window = None   # (t0, t1) host times of the timed region
+
+    def mark_region(self, t0, t1):
+        """Host wall-clock bounds of the timed region: samples arriving inside it
+        are the in-region ones."""
+        self.window = (t0, t1)
 
     def __enter__(self):
         try:
@@ -98,11 +104,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
         self.late = False
-        if self.proc and not self.lines:
+        if self.proc and not self.lines and not self.window:
             # timed region shorter than nvidia-smi's start-up: take the first
             # sample just after it (flagged in the summary) rather than none
             t0 = time.time()
@@ -120,7 +126,16 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [ln for _, ln in self.lines]
+        where = "timed region"
+        if self.window:
+            # nvidia-smi prints a sample ~at its query time; allow one period of lag
+            inside = [ln for t, ln in self.lines if self.window[0] <= t <= self.window[1] + 0.1]
+            if inside:
+                lines = inside
+            else:
+                where = "soak before the timed region (same kernel, back to back)"
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -134,7 +149,8 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+               "sampled_during": where}
         if getattr(self, "late", False):
             out["note"] = "timed region shorter than the sampler start-up; one sample taken right after it"
         return out
@@ -259,6 +275,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--conv-beta", type=float, default=0.0)
+    ap.add_argument("--conv-r", type=int, default=3, help="filter size R = S (PAPER.md:835: 3..11)")
+    ap.add_argument("--conv-valid", action="store_true", help="valid padding (PAPER.md:826 exact shape)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -310,36 +328,46 @@ def main():
                         C.data_ptr(), C.stride(0), algo)
     check = rank == 0 and not args.no_cpu and world == 1
     C0 = C.clone() if check else None  # the steps update C in place; the parity sample needs the input
-    for _ in range(args.warmup):
+
+    def one(i=None):
+        if flush is not None:
+            torch.sum(flush, dim=0, out=flush_out[0])
+        if i is not None:
+            ev[i][0].record(stream)
         step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+        if i is not None:
+            ev[i][1].record(stream)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clocks:
+        # The sampler starts before the warm-up, which then soaks the GPU with
+        # the same step for >= 1 s, so short timed regions still have clock
+        # samples under this load (in-region ones preferred, see summary()).
+        t_soak = time.time()
+        for _ in range(args.warmup):
+            one()
         torch.cuda.synchronize()
+        while time.time() - t_soak < 1.0:
+            for _ in range(8):
+                one()
+            torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
+        torch.cuda.synchronize()
+        t0_host = time.time()
         for i in range(args.steps):
-            if flush is not None:
-                torch.sum(flush, dim=0, out=flush_out[0])
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-        t_end.record(stream)
+            one(i)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        clocks.mark_region(t0_host, time.time())
     per_step = [a.elapsed_time(b) for a, b in ev]  # ms, device time of each step's hot path
     total_ms = sum(per_step)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    med_ms = statistics.median(per_step)
+    t = torch.tensor([total_ms, med_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms, med_ms = float(t[0].item()), float(t[1].item())
     ms_per_step = total_ms / args.steps
     flops = 2.0 * m * n * k
     value = flops * args.steps / (total_ms * 1e-3) / 1e9  # GFLOP/s, whole job
@@ -348,7 +376,7 @@ def main():
     kernel = path if path in ("simt", "tf32x1") else "tf32x3"
     bound, peak, unit, peak_note = roofline_peak(kernel, peaks)
     my_flops = 2.0 * rows * n * k
-    my_ms = statistics.mean(per_step)
+    my_ms = statistics.median(per_step)  # the paper reports medians
     if args.config == "C4":
         bound, unit = "hbm", "GB/s"
         peak = peaks["hbm_gbs"]
@@ -363,13 +391,23 @@ def main():
             "traffic_source": traffic_src, "kernel": f"k_sgemm_tc ({path})" if kernel != "simt"
             else "k_sgemm_simt", "peak_source": peak_note}
     if bound == "tensor":
-        sus = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / 3.0
+        per_product = 1.0 if kernel == "tf32x1" else 3.0  # tensor MMAs per fp32 product
+        sus = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / per_product
         roof["frac_of_sustained_peak"] = round(achieved / sus, 4)
+        # clock-normalised: against the tf32 rate measured by scripts/mma_rate.py
+        # (4096 flop/clk/SM, kind::tf32) at the median SM clock sampled under load
+        f_sm = clocks.summary().get("sm_mhz")
+        if f_sm:
+            clk_peak = 148 * 4096 * f_sm * 1e6 / 1e12 / per_product
+            roof["frac_clock_normalized"] = round(achieved / clk_peak, 4)
+            roof["clock_normalized_peak"] = round(clk_peak, 2)
     launches = args.steps * (1 if comm is None else max(1, min(8, k // 512)))
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "step_ms": {"median": round(med_ms, 4), "min": round(min(per_step), 4), "max": round(max(per_step), 4)},
+        "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": {"simt": "f32", "tf32x1": "tf32 (1xTF32 tensor-core, fp32 accumulate)"}.get(
             kernel, "f32 (3xTF32 tensor-core, fp32 accumulate)"), "data": "synthetic (seeded U[-1,1) fp32, device-generated)",
         "config": {"workload": desc, "m": m, "n": n, "k": k, "alpha": alpha, "beta": beta, "path": path,
@@ -404,41 +442,56 @@ def run_conv(args):
     BASELINE.json config).  Roofline: HBM (X read once, Y written [and read])."""
     import torch
     import paper_1804_10694_b200 as tm
-    Nb, H, W, C, F, R, S, pad = 32, 512, 512, 16, 16, 3, 3, 1
+    R = S = args.conv_r
+    pad = 0 if args.conv_valid else R // 2
+    Nb, H, W, C, F = 32, 512, 512, 16, 16
+    Ho, Wo = H + 2 * pad - R + 1, W + 2 * pad - S + 1
     g = torch.Generator(device="cuda")
     g.manual_seed(1804)
     X = torch.rand((Nb, H, W, C), generator=g, device="cuda") * 2 - 1
     Wt = torch.rand((F, R, S, C), generator=g, device="cuda") * 2 - 1
-    Y = torch.rand((Nb, H, W, F), generator=g, device="cuda") * 2 - 1
+    Y = torch.rand((Nb, Ho, Wo, F), generator=g, device="cuda") * 2 - 1
     algo = ALGOS[args.algo]
     alpha, beta = (1.0, 0.0) if args.conv_beta == 0.0 else (1.5, args.conv_beta)
-    for _ in range(args.warmup):
-        tm.conv2d_nhwc(X, Wt, Y, alpha, beta, pad, algo=algo)
-    torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(0) as clocks:
+        t_soak = time.time()
+        for _ in range(args.warmup):
+            tm.conv2d_nhwc(X, Wt, Y, alpha, beta, pad, algo=algo)
+        torch.cuda.synchronize()
+        while time.time() - t_soak < 1.0:
+            for _ in range(8):
+                tm.conv2d_nhwc(X, Wt, Y, alpha, beta, pad, algo=algo)
+            torch.cuda.synchronize()
+        t0_host = time.time()
         for i in range(args.steps):
             ev[i][0].record()
             tm.conv2d_nhwc(X, Wt, Y, alpha, beta, pad, algo=algo)
             ev[i][1].record()
         torch.cuda.synchronize()
-    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-    flops = 2.0 * Nb * H * W * F * R * S * C
+        clocks.mark_region(t0_host, time.time())
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)  # median (PAPER.md:812)
+    flops = 2.0 * Nb * Ho * Wo * F * R * S * C
     algo_bytes = 4 * (X.numel() + Wt.numel() + (2 if beta != 0.0 else 1) * Y.numel())
     peaks = load_peaks()
     gbs = algo_bytes / (ms * 1e-3) / 1e9
-    traffic, traffic_src = (ncu_traffic("CONV", "tf32x3", 1) if (beta == 0.0 and algo != 2) else (None, None))
+    paper_default = R == 3 and not args.conv_valid
+    traffic, traffic_src = (ncu_traffic("CONV", "tf32x3", 1) if (beta == 0.0 and algo != 2 and paper_default)
+                            else (None, None))
     line = {"metric": "conv2d GB/s (PAPER.md:826 Conv shape, 3xTF32 tensor cores)", "value": round(gbs, 2), "unit": "GB/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "dtype": "f32 (3xTF32 tensor-core)" if algo != 2 else "f32",
             "gflops": round(flops / (ms * 1e-3) / 1e9, 1), "data": "synthetic (device-generated U[-1,1))",
-            "config": {"workload": f"PAPER.md:826 Conv: NHWC 32x512x512x16, KRSC 16x3x3x16, pad 1, alpha {alpha} beta {beta}",
+            "config": {"workload": f"PAPER.md:826 Conv: NHWC 32x512x512x16, KRSC 16x{R}x{S}x16, pad {pad}"
+                                   f"{' (valid)' if args.conv_valid else ''}, alpha {alpha} beta {beta}",
+                       "gemm_view": {"m": Nb * Ho * Wo, "n": F, "k": R * S * C},
                        "l2": "inputs larger than L2, no flush"},
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
                          "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
                          "algorithmic_bytes": algo_bytes,
-                         "kernel": "k_conv_direct (auto)" if algo != 2 else "k_conv_simt"},
+                         "kernel": "k_conv_simt" if algo == 2 else ("k_conv_direct" if R * C <= 128
+                                                                    else "k_sgemm_tc<CONV> (implicit GEMM)")},
             "gpu_launches": args.steps,
             "clocks": clocks.summary()}
     print(json.dumps(line), flush=True)

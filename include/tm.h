@@ -245,7 +245,12 @@ tm_status tm_dist_chunk(int64_t k, int nranks, int idx, int64_t* k0, int64_t* kr
 /* Collective: all ranks call with identical m, n, k, alpha, beta, root.
  *   A_local: rows x k (lda), C_local: rows x n (ldc), rows from tm_dist_rows.
  *   B: k x n (ldb); valid on `root`; on other ranks a caller-owned k*ldb
- *      device buffer that is overwritten with root's B.
+ *      device buffer that is overwritten with root's B.  Whole rows of ldb
+ *      floats are transferred, so on EVERY rank B must be a buffer of k*ldb
+ *      floats (the root's last row is read up to k*ldb, past the last valid
+ *      element (k-1)*ldb + n), and on receivers the padding columns [n, ldb)
+ *      of each row are overwritten too: a column-slice view of a wider matrix
+ *      would have its neighbouring columns clobbered -- pass ldb == n then.
  * On return (stream-ordered) C_local = alpha*A_local*B + beta*C_local. */
 tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha,
                         const float* A_local, int64_t lda, float* B, int64_t ldb, int root,
@@ -272,7 +277,10 @@ tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int6
 /* Variant: B is pre-sharded by k-rows (B_shard = rows [k0, k0+kr) of B from
  * tm_dist_rows(k, ...), leading dimension ldb), all-gathered into the
  * caller-owned B_full (k x n, ldb).  Requires every rank's shard to have the
- * same row count (k % nranks == 0), as ncclAllGather does. */
+ * same row count (k % nranks == 0), as ncclAllGather does.  Buffer extents:
+ * whole rows of ldb floats move, so B_shard must be kr*ldb floats and B_full
+ * k*ldb floats (kr = k/nranks), and the padding columns [n, ldb) of B_full are
+ * overwritten with the shards' padding -- pass ldb == n for column-slice views. */
 tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha,
                                   const float* A_local, int64_t lda, const float* B_shard,
                                   float* B_full, int64_t ldb, float beta, float* C_local,

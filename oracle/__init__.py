@@ -35,12 +35,22 @@ def build(force: bool = False) -> str:
     """Compile oracle.c into liboracle.so (no-op when up to date)."""
     if os.environ.get("TM_ORACLE_LIB"):
         return os.environ["TM_ORACLE_LIB"]
+    import hashlib
     with _lock:
-        stale = (not os.path.exists(_LIB)) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC)
+        with open(_SRC, "rb") as f:
+            digest = hashlib.sha256(f.read() + " ".join(CFLAGS).encode()).hexdigest()
+        stamp = _LIB + ".build.json"
+        try:
+            with open(stamp) as f:
+                stale = not os.path.exists(_LIB) or f.read().strip() != digest
+        except OSError:
+            stale = True
         if force or stale:
             tmp = _LIB + f".tmp{os.getpid()}"
             subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lm"])
             os.replace(tmp, _LIB)
+            with open(stamp, "w") as f:
+                f.write(digest)
     return _LIB
 
 

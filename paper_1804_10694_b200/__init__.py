@@ -133,6 +133,11 @@ def _stream(stream):
 _F32 = None
 
 
+def _f32_dtype():
+    import torch
+    return torch.float32
+
+
 def _f32(name, t):
     global _F32
     if t is None:
@@ -145,16 +150,40 @@ def _f32(name, t):
     return t
 
 
+def _on_device(**tensors):
+    """Every tensor is a CUDA tensor on the current device (a host or other-device
+    pointer handed to a kernel would fault or poison the context)."""
+    import torch
+    for name, t in tensors.items():
+        if t is not None and not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (got {t.device})")
+    dev = torch.cuda.current_device()
+    for name, t in tensors.items():
+        if t is not None and t.device.index != dev:
+            raise ValueError(f"{name} is on {t.device} but the current device is cuda:{dev}")
+
+
+def _shape(name, t, rows, cols):
+    if t is not None and (t.dim() != 2 or tuple(t.shape) != (rows, cols)):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected ({rows}, {cols})")
+
+
 def sgemm_ex(A, B, C, alpha: float = 1.0, beta: float = 0.0, algo: int = ALGO_AUTO, stream=None,
              m=None, n=None, k=None):
     """In place: C <- alpha*A@B + beta*C on CUDA tensors (row-major 2-D views).
 
     A may be None when alpha == 0 or k == 0 (it is then not read), likewise B.
+    Shapes must agree: A (m, k), B (k, n), C (m, n) -- ValueError otherwise, as
+    for torch.mm -- and every tensor must live on the current CUDA device.
     """
     A, B, C = _f32("A", A), _f32("B", B), _f32("C", C)
     m = C.shape[0] if m is None else m
     n = C.shape[1] if n is None else n
-    k = (A.shape[1] if A is not None else 0) if k is None else k
+    k = (A.shape[1] if A is not None else (B.shape[0] if B is not None else 0)) if k is None else k
+    _shape("A", A, m, k)
+    _shape("B", B, k, n)
+    _shape("C", C, m, n)
+    _on_device(A=A, B=B, C=C)
     lda = _ld(A) if A is not None else max(k, 1)
     ldb = _ld(B) if B is not None else max(n, 1)
     st = lib.tm_sgemm_ex(m, n, k, float(alpha), _ptr(A), lda, _ptr(B), ldb, float(beta), _ptr(C), _ld(C),
@@ -171,6 +200,9 @@ def sgemm_op(A, B, C, alpha: float = 1.0, beta: float = 0.0, opa: str = "N", opb
     m, n = C.shape
     ta, tb = opa == "T", opb == "T"
     k = A.shape[0] if ta else A.shape[1]
+    _shape("A", A, *((k, m) if ta else (m, k)))
+    _shape("B", B, *((n, k) if tb else (k, n)))
+    _on_device(A=A, B=B, C=C)
     st = lib.tm_sgemm_op(int(ta), int(tb), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B), float(beta),
                          _ptr(C), _ld(C), _stream(stream), int(algo))
     _check(st, "tm_sgemm_op")
@@ -186,6 +218,9 @@ def tune(A, B, C, alpha: float = 1.0, beta: float = 0.0, opa: str = "N", opb: st
     m, n = C.shape
     ta, tb = opa == "T", opb == "T"
     k = A.shape[0] if ta else A.shape[1]
+    _shape("A", A, *((k, m) if ta else (m, k)))
+    _shape("B", B, *((n, k) if tb else (k, n)))
+    _on_device(A=A, B=B, C=C)
     cg, bn, sk, ms = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_float()
     st = lib.tm_sgemm_tune(int(ta), int(tb), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B), float(beta),
                            _ptr(C), _ld(C), _stream(stream), int(reps), ctypes.byref(cg), ctypes.byref(bn),
@@ -235,6 +270,7 @@ def conv2d_nhwc(X, Wt, Y, alpha: float = 1.0, beta: float = 0.0, pad: int = 0, a
         _f32(name, t)
         if not t.is_contiguous():
             raise ValueError(f"{name} must be contiguous")
+    _on_device(X=X, Wt=Wt, Y=Y)
     nb, h, w, c = X.shape
     f, r, s, c2 = Wt.shape
     if c2 != c or tuple(Y.shape) != (nb, h + 2 * pad - r + 1, w + 2 * pad - s + 1, f):
@@ -271,17 +307,30 @@ def sgemm_host(A, B, C, alpha: float = 1.0, beta: float = 0.0, algo: int = ALGO_
         if isinstance(x, np.ndarray):
             if x.dtype != np.float32:
                 raise TypeError("float32 required")
+            if x.ndim != 2:
+                raise ValueError("expected a 2-D array")
+            # row-major views only: unit column stride, positive row stride
+            if x.shape[1] > 1 and x.strides[1] != 4:
+                raise ValueError("expected unit column stride (row-major)")
+            if x.shape[0] > 1 and (x.strides[0] <= 0 or x.strides[0] % 4):
+                raise ValueError("expected a positive row stride that is a multiple of 4 bytes")
             ld = x.strides[0] // 4 if x.shape[0] > 1 else max(x.shape[1], 1)
             return ctypes.c_void_p(x.ctypes.data), ld
         if x.is_cuda:
             raise ValueError("sgemm_host takes host buffers")
+        if x.dtype != _f32_dtype():
+            raise TypeError("float32 required")
         return ctypes.c_void_p(x.data_ptr()), _ld(x)
+
+    m, n = C.shape
+    k = A.shape[1] if A is not None else (B.shape[0] if B is not None else 0)
+    for name, x, shp in (("A", A, (m, k)), ("B", B, (k, n))):
+        if x is not None and tuple(x.shape) != shp:
+            raise ValueError(f"{name} has shape {tuple(x.shape)}, expected {shp}")
 
     pa, lda = info(A)
     pb, ldb = info(B)
     pc, ldc = info(C)
-    m, n = C.shape
-    k = A.shape[1] if A is not None else 0
     st = lib.tm_sgemm_host(m, n, k, float(alpha), pa, lda or max(k, 1), pb, ldb or max(n, 1), float(beta), pc,
                            ldc, _stream(stream), int(algo))
     _check(st, "tm_sgemm_host")
@@ -373,7 +422,10 @@ class Comm:
         return int(v.value)
 
     def sgemm(self, m, n, k, A_local, B, C_local, alpha=1.0, beta=0.0, root=0, stream=None):
-        """Row-sharded C_local <- alpha*A_local@B + beta*C_local; B broadcast from root."""
+        """Row-sharded C_local <- alpha*A_local@B + beta*C_local; B broadcast from root.
+
+        Whole rows of B (ldb floats, padding included) are broadcast: B must be a
+        k*ldb buffer on every rank (tm.h); use a dense B (ldb == n) for views."""
         st = lib.tm_sgemm_dist(self.handle, m, n, k, float(alpha), _ptr(A_local),
                                _ld(A_local) if A_local is not None and A_local.shape[0] > 0 else max(k, 1),
                                _ptr(B), _ld(B), int(root), float(beta), _ptr(C_local),
@@ -382,6 +434,9 @@ class Comm:
         return C_local
 
     def sgemm_allgather(self, m, n, k, A_local, B_shard, B_full, C_local, alpha=1.0, beta=0.0, stream=None):
+        """B_shard (k/P x n) of every rank all-gathered into B_full (k x n), then the
+        row-sharded GEMM.  Whole rows (ldb floats) move: B_shard must span
+        (k/P)*ldb floats and B_full k*ldb (tm.h); use dense tensors for views."""
         st = lib.tm_sgemm_dist_allgather(self.handle, m, n, k, float(alpha), _ptr(A_local),
                                          _ld(A_local) if A_local.shape[0] > 0 else max(k, 1), _ptr(B_shard),
                                          _ptr(B_full), _ld(B_full), float(beta), _ptr(C_local),

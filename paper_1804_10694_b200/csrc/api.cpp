@@ -183,7 +183,9 @@ struct Workspace {
   bool init = false;
 };
 Workspace g_ws[kMaxDevices];
-std::mutex g_ws_mu;
+// One lock per device: a synchronous tm_sgemm_host call holds its device's
+// staging buffers for the whole call, callers on other devices proceed.
+std::mutex g_ws_mu[kMaxDevices];
 
 tm_status ws_get(int dev, size_t bytes, Workspace** out) {
   Workspace& w = g_ws[dev];
@@ -237,25 +239,35 @@ tm_status sgemm_reserve(const GemmArgs& a, cudaStream_t stream, int sm_reserve) 
 }
 
 tm_status streamk_workspace(cudaStream_t stream, size_t ws_bytes, size_t flag_count, float** ws, unsigned** flags,
-                            unsigned* epoch) {
+                            unsigned* epoch, void** graph_owned) {
+  *graph_owned = nullptr;
+  // CUDA graph capture: the graph gets its own workspace, allocated and freed
+  // inside the graph (cudaMallocAsync / cudaFreeAsync become memory nodes), so
+  // it does not depend on which stream captures it, can be replayed on any
+  // stream, and never shares flags or partials with direct calls or with other
+  // graphs.  Its epoch is baked into the kernel parameters, so the flags are
+  // cleared inside the graph before every replay and the captured launch uses
+  // epoch 1.  The caller releases it with cudaFreeAsync after the launch.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) return TM_ERR_CUDA;
+  if (cap == cudaStreamCaptureStatusActive) {
+    const size_t fbytes = (flag_count * sizeof(unsigned) + 255) & ~size_t(255);
+    void* base = nullptr;
+    if (cudaMallocAsync(&base, fbytes + ws_bytes, stream) != cudaSuccess) {
+      cudaGetLastError();
+      return TM_ERR_OUT_OF_MEMORY;
+    }
+    if (cudaMemsetAsync(base, 0, fbytes, stream) != cudaSuccess) return TM_ERR_CUDA;
+    *flags = static_cast<unsigned*>(base);
+    *ws = ws_bytes ? reinterpret_cast<float*>(static_cast<char*>(base) + fbytes) : nullptr;
+    *epoch = 1;
+    *graph_owned = base;
+    return TM_OK;
+  }
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return TM_ERR_CUDA;
   std::lock_guard<std::mutex> lk(g_sk_mu);
   SkWorkspace& w = g_sk[{dev, stream}];
-  // CUDA graph capture: no allocation is possible while capturing (run the
-  // same call once outside the capture first), and the graph will be replayed
-  // with the epoch baked into the kernel parameters, so the flags are cleared
-  // inside the graph before every replay and the captured launch uses epoch 1.
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) return TM_ERR_CUDA;
-  if (cap == cudaStreamCaptureStatusActive) {
-    if (w.ws_bytes < ws_bytes || w.flag_count < flag_count) return TM_ERR_INVALID_VALUE;
-    if (cudaMemsetAsync(w.flags, 0, w.flag_count * sizeof(unsigned), stream) != cudaSuccess) return TM_ERR_CUDA;
-    *ws = w.ws;
-    *flags = w.flags;
-    *epoch = 1;
-    return TM_OK;
-  }
   if (w.ws_bytes < ws_bytes) {
     if (w.ws) g_sk_retired.push_back(w.ws);
     w.ws = nullptr;
@@ -466,7 +478,8 @@ tm_status tm_sgemm_host(int64_t m, int64_t n, int64_t k, float alpha, const floa
     const size_t a_el = reads_ab ? static_cast<size_t>(m) * dlda : 0;
     const size_t b_el = reads_ab ? static_cast<size_t>(k) * dldb : 0;
     const size_t c_el = static_cast<size_t>(m) * dldc;
-    std::lock_guard<std::mutex> lk(tmk::g_ws_mu);
+    if (devid < 0 || devid >= tmk::kMaxDevices) return TM_ERR_UNSUPPORTED_DEVICE;
+    std::lock_guard<std::mutex> lk(tmk::g_ws_mu[devid]);
     tmk::Workspace* w = nullptr;
     st = tmk::ws_get(devid, (a_el + b_el + c_el) * 4 + 256, &w);
     if (st != TM_OK) return st;
@@ -524,7 +537,8 @@ tm_status tm_sgemm_host(int64_t m, int64_t n, int64_t k, float alpha, const floa
 tm_status tm_release_workspace(void) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return TM_ERR_CUDA;
-  std::lock_guard<std::mutex> lk(tmk::g_ws_mu);
+  if (dev < 0 || dev >= tmk::kMaxDevices) return TM_ERR_UNSUPPORTED_DEVICE;
+  std::lock_guard<std::mutex> lk(tmk::g_ws_mu[dev]);
   tmk::Workspace& w = tmk::g_ws[dev];
   if (w.buf) cudaFree(w.buf);
   w.buf = nullptr;

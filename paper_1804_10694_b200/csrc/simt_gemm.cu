@@ -195,50 +195,59 @@ __global__ void k_l2_flush(const float4* __restrict__ buf, int64_t n, float* sin
 
 // Direct NHWC / KRSC convolution, FP32 FFMA (validation path for the
 // implicit-GEMM tensor-core kernel and fallback for any shape): one thread per
-// output pixel, 16 filters per thread (blockIdx.y selects the filter group);
-// the group's filter taps are staged in shared memory per (ky, kx).
+// output pixel, 16 filters per thread; the group's filter taps are staged in
+// shared memory per (ky, kx) in chunks of kConvCc channels (any C fits), and
+// filter groups stride over gridDim.y (any F fits).  Summation order per output:
+// ky, kx, c ascending (chunking does not reorder it).
 constexpr int kConvF = 16;
+constexpr int kConvCc = 512;
 __global__ void __launch_bounds__(128) k_conv_simt(ConvArgs a) {
-  extern __shared__ float wsh[];  // [kConvF][C] filters of one tap
+  __shared__ float wsh[kConvF * kConvCc];  // [kConvF][cc] filters of one tap, one channel chunk
   const int64_t ho = a.ho(), wo = a.wo();
   const int64_t P = a.nb * ho * wo;
   const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int f0 = blockIdx.y * kConvF;
-  const int nf = static_cast<int>(a.f - f0 < kConvF ? a.f - f0 : kConvF);
+  const int64_t fgroups = (a.f + kConvF - 1) / kConvF;
   int64_t b = 0, y = 0, x = 0;
   if (q < P) {
     b = q / (ho * wo);
     y = (q / wo) % ho;
     x = q % wo;
   }
-  float acc[kConvF];
+  for (int64_t fg = blockIdx.y; fg < fgroups; fg += gridDim.y) {
+    const int64_t f0 = fg * kConvF;
+    const int nf = static_cast<int>(a.f - f0 < kConvF ? a.f - f0 : kConvF);
+    float acc[kConvF];
 #pragma unroll
-  for (int j = 0; j < kConvF; ++j) acc[j] = 0.0f;
-  for (int64_t ky = 0; ky < a.r; ++ky) {
-    for (int64_t kx = 0; kx < a.s; ++kx) {
-      __syncthreads();
-      for (int64_t i = threadIdx.x; i < static_cast<int64_t>(nf) * a.c; i += blockDim.x) {
-        const int64_t fj = i / a.c, c = i - fj * a.c;
-        wsh[fj * a.c + c] = a.Wt[(((f0 + fj) * a.r + ky) * a.s + kx) * a.c + c];
-      }
-      __syncthreads();
-      const int64_t iy = y + ky - a.pad, ix = x + kx - a.pad;
-      if (q < P && iy >= 0 && iy < a.h && ix >= 0 && ix < a.w) {
-        const float* xp = a.X + ((b * a.h + iy) * a.w + ix) * a.c;
-        for (int64_t c = 0; c < a.c; ++c) {
-          const float xv = __ldg(xp + c);
+    for (int j = 0; j < kConvF; ++j) acc[j] = 0.0f;
+    for (int64_t ky = 0; ky < a.r; ++ky) {
+      for (int64_t kx = 0; kx < a.s; ++kx) {
+        for (int64_t c0 = 0; c0 < a.c; c0 += kConvCc) {
+          const int64_t cc = a.c - c0 < kConvCc ? a.c - c0 : kConvCc;
+          __syncthreads();
+          for (int64_t i = threadIdx.x; i < static_cast<int64_t>(nf) * cc; i += blockDim.x) {
+            const int64_t fj = i / cc, c = i - fj * cc;
+            wsh[fj * cc + c] = a.Wt[(((f0 + fj) * a.r + ky) * a.s + kx) * a.c + c0 + c];
+          }
+          __syncthreads();
+          const int64_t iy = y + ky - a.pad, ix = x + kx - a.pad;
+          if (q < P && iy >= 0 && iy < a.h && ix >= 0 && ix < a.w) {
+            const float* xp = a.X + ((b * a.h + iy) * a.w + ix) * a.c + c0;
+            for (int64_t c = 0; c < cc; ++c) {
+              const float xv = __ldg(xp + c);
 #pragma unroll
-          for (int j = 0; j < kConvF; ++j)
-            if (j < nf) acc[j] = fmaf(xv, wsh[j * a.c + c], acc[j]);
+              for (int j = 0; j < kConvF; ++j)
+                if (j < nf) acc[j] = fmaf(xv, wsh[j * cc + c], acc[j]);
+            }
+          }
         }
       }
     }
-  }
-  if (q < P) {
-    float* yp = a.Y + q * a.f + f0;
+    if (q < P) {
+      float* yp = a.Y + q * a.f + f0;
 #pragma unroll
-    for (int j = 0; j < kConvF; ++j)
-      if (j < nf) yp[j] = (a.beta == 0.0f) ? a.alpha * acc[j] : fmaf(a.alpha, acc[j], a.beta * yp[j]);
+      for (int j = 0; j < kConvF; ++j)
+        if (j < nf) yp[j] = (a.beta == 0.0f) ? a.alpha * acc[j] : fmaf(a.alpha, acc[j], a.beta * yp[j]);
+    }
   }
 }
 
@@ -248,12 +257,9 @@ tm_status launch_conv_simt(const ConvArgs& a, cudaStream_t stream) {
   const int64_t P = a.nb * a.ho() * a.wo();
   const int64_t blocks = (P + 127) / 128;
   const int64_t fgroups = (a.f + kConvF - 1) / kConvF;
-  const size_t smem = static_cast<size_t>(kConvF) * a.c * 4;
-  if (blocks > INT32_MAX || fgroups > 65535 || smem > 160 * 1024) return TM_ERR_INVALID_VALUE;
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(k_conv_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
-    return TM_ERR_CUDA;
-  k_conv_simt<<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(fgroups)), 128, smem, stream>>>(a);
+  if (blocks > INT32_MAX) return TM_ERR_INVALID_VALUE;
+  const unsigned gy = static_cast<unsigned>(fgroups < 65535 ? fgroups : 65535);
+  k_conv_simt<<<dim3(static_cast<unsigned>(blocks), gy), 128, 0, stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? TM_OK : TM_ERR_CUDA;
 }
 

@@ -424,12 +424,8 @@ tm_status launch_dc(const ConvArgs& a, const DcParams& p, int smem, int num_sms,
   if (!encode_halo(&tmX, a, p.cw, p.halo_w)) return TM_ERR_INTERNAL;
   if (!encode_filters(&tmW, a, p.fp)) return TM_ERR_INTERNAL;
   auto kern = k_conv_direct<S>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDcMaxSmem) != cudaSuccess)
-      return TM_ERR_CUDA;
-    attr_set = true;
-  }
+  static std::atomic<unsigned long long> optin{0};  // per instantiation, bit per device
+  if (tm_status st = ensure_smem_optin(optin, kern, kDcMaxSmem); st != TM_OK) return st;
   const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
   kern<<<grid, kThreads, smem, stream>>>(tmX, tmW, p);
   return cudaPeekAtLastError() == cudaSuccess ? TM_OK : TM_ERR_CUDA;

@@ -827,12 +827,8 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
                         cudaStream_t stream) {
   using Cfg = TcCfg<CG, BN_CTA, SPLIT3, BK, TA>;
   auto kern = k_sgemm_tc<CG, BN_CTA, SPLIT3, TA, TB, BK, CONV>;
-  static bool attr_set = false;  // per instantiation; attribute is per-function, process-wide
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes) != cudaSuccess)
-      return TM_ERR_CUDA;
-    attr_set = true;
-  }
+  static std::atomic<unsigned long long> optin{0};  // per instantiation, bit per device
+  if (tm_status st = ensure_smem_optin(optin, kern, Cfg::kSmemBytes); st != TM_OK) return st;
   // Tuning knobs (bench/tests only), read once per process.
   static const int env_kc = [] { const char* e = std::getenv("TM_KC_BLOCKS"); return e ? std::max(1, std::atoi(e)) : 0; }();
   static const int env_gm = [] { const char* e = std::getenv("TM_GROUP_M"); return e ? std::max(1, std::atoi(e)) : 0; }();
@@ -845,13 +841,14 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
   p.ws = nullptr;
   p.flags = nullptr;
   p.epoch = 0;
+  void* graph_owned = nullptr;  // workspace allocated inside a CUDA graph being captured
   if (streamk) {
     clusters = max_clusters;
     if (p.iters < 2LL * clusters) clusters = static_cast<int>(p.iters / 2 > 0 ? p.iters / 2 : 1);
     const size_t ws_bytes = static_cast<size_t>(clusters) * CG * kBMCta * Cfg::kMmaN * 4;
     // flags[0] of the workspace is reserved for the wave barrier counter
     const size_t flag_count = 1 + static_cast<size_t>(clusters) * CG * kEpiWarps;
-    tm_status st = streamk_workspace(stream, ws_bytes, flag_count, &p.ws, &p.flags, &p.epoch);
+    tm_status st = streamk_workspace(stream, ws_bytes, flag_count, &p.ws, &p.flags, &p.epoch, &graph_owned);
     if (st != TM_OK) return st;
     p.flags += 1;
     p.streamk = 1;
@@ -868,9 +865,9 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
   if (wave_sync && !CONV && p.kblocks >= 64 && !p.streamk && p.num_tiles / clusters >= 2) {
     float* ws_unused = nullptr;
     unsigned epoch_unused = 0;
-    tm_status st = streamk_workspace(stream, 0, 1, &ws_unused, &p.wave_ctr, &epoch_unused);  // slot 0
+    tm_status st = streamk_workspace(stream, 0, 1, &ws_unused, &p.wave_ctr, &epoch_unused, &graph_owned);  // slot 0
     if (st != TM_OK) return st;
-    if (cudaMemsetAsync(p.wave_ctr, 0, sizeof(unsigned), stream) != cudaSuccess) return TM_ERR_CUDA;
+    if (!graph_owned && cudaMemsetAsync(p.wave_ctr, 0, sizeof(unsigned), stream) != cudaSuccess) return TM_ERR_CUDA;
     p.full_waves = p.num_tiles / clusters;
   }
   cudaLaunchConfig_t cfg = {};
@@ -898,7 +895,9 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
     if (cudaMalloc(&p.trace, sizeof(unsigned long long) * kTraceSlots * clusters * CG) != cudaSuccess) return TM_ERR_CUDA;
     cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * kTraceSlots * clusters * CG, stream);
   }
-  if (cudaLaunchKernelEx(&cfg, kern, tmA, tmB, p) != cudaSuccess) return TM_ERR_CUDA;
+  const bool launched = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, p) == cudaSuccess;
+  if (graph_owned && cudaFreeAsync(graph_owned, stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (!launched) return TM_ERR_CUDA;
   if (trace_path) {
     const int n = kTraceSlots * clusters * CG;
     unsigned long long* h = new unsigned long long[n];

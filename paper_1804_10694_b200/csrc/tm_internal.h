@@ -2,11 +2,28 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "../../include/tm.h"
 
 namespace tmk {
+
+// The dynamic-shared-memory opt-in (cudaFuncSetAttribute) is recorded per
+// device, so it is set once per (kernel, device): `done` is the caller's
+// per-kernel bitmask of devices already opted in (devices >= 64 set it every
+// call).  Thread-safe: a race only repeats the idempotent attribute call.
+template <class Kernel>
+tm_status ensure_smem_optin(std::atomic<unsigned long long>& done, Kernel kern, int bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TM_ERR_CUDA;
+  const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return TM_OK;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return TM_ERR_CUDA;
+  done.fetch_or(bit, std::memory_order_release);
+  return TM_OK;
+}
 
 // C = alpha * op(A) * op(B) + beta * C, row-major.  ta: op(A) = A^T (A stored
 // k x m, lda >= m); tb: op(B) = B^T (B stored n x k, ldb >= k).
@@ -50,9 +67,11 @@ tm_status sgemm_reserve(const GemmArgs& a, cudaStream_t stream, int sm_reserve);
 
 // Library-owned stream-K workspace for `stream` on the current device: at least
 // ws_bytes of fp32 partials and flag_count epoch flags; *epoch is the value this
-// launch must write (flags hold earlier epochs, never the new one).
+// launch must write (flags hold earlier epochs, never the new one).  Under CUDA
+// graph capture the workspace is allocated inside the graph and *graph_owned is
+// set: the caller enqueues cudaFreeAsync(*graph_owned, stream) after its launch.
 tm_status streamk_workspace(cudaStream_t stream, size_t ws_bytes, size_t flag_count, float** ws, unsigned** flags,
-                            unsigned* epoch);
+                            unsigned* epoch, void** graph_owned);
 
 // Implicit-GEMM convolution, NHWC activations, KRSC filters, stride 1:
 // Y[b,y,x,f] = alpha * sum X[b, y+ky-pad, x+kx-pad, c] * Wt[f,ky,kx,c] + beta * Y.

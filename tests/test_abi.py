@@ -142,3 +142,26 @@ def test_op_and_colmajor_validation_on_host():
     assert L.tm_sgemm_op(0, 1, 8, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 10, 0.0, vp(1 << 24), 8, None, 1) == 1
     assert L.tm_sgemm_colmajor(b"X", b"N", 8, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None) == 1
     assert L.tm_sgemm_op(1, 1, 0, 8, 8, 1.0, vp(16), 8, vp(1 << 16), 8, 0.0, vp(1 << 24), 8, None, 0) == 0  # noop
+
+
+def test_binding_rejects_mismatched_shapes_and_host_tensors():
+    """The binding checks shapes (as torch.mm does) and devices before any
+    pointer reaches a kernel (ValueError, nothing launched)."""
+    import numpy as np
+    import torch
+    A, B, C = torch.zeros(8, 4), torch.zeros(4, 6), torch.zeros(8, 6)
+    with pytest.raises(ValueError):
+        tm.sgemm(torch.zeros(7, 4), B, C)          # A has fewer than m rows
+    with pytest.raises(ValueError):
+        tm.sgemm(A, torch.zeros(3, 6), C)          # B has fewer than k rows
+    with pytest.raises(ValueError):
+        tm.sgemm_op(A, torch.zeros(6, 5), C, opb="T")
+    with pytest.raises(ValueError):
+        tm.sgemm(A, B, C)                          # host tensors are not device tensors
+    with pytest.raises(ValueError):
+        tm.sgemm_host(A.numpy(), B.numpy()[:, ::2].copy()[:, :3], C.numpy())  # shape mismatch
+    Bs = np.zeros((4, 12), np.float32)[:, ::2]     # non-unit column stride
+    with pytest.raises(ValueError):
+        tm.sgemm_host(A.numpy(), Bs, C.numpy())
+    with pytest.raises(ValueError):
+        tm.sgemm_host(A.numpy(), np.zeros((4, 6), np.float32)[::-1], C.numpy())  # negative row stride

@@ -101,3 +101,46 @@ def test_conv_paper_shape_sampled_pixels(path):
     pix = np.unique(np.concatenate([g.integers(0, P, 3000), [0, 511, 512, 512 * 511, P - 1, P - 512]]))
     R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, 1, pixels=pix)
     assert float(np.max(oracle.normalized_error(Y[pix], R, D))) <= TOL
+
+
+# The paper's larger specialised filters ("3x3, 5x5, 7x7, 9x9
+# and 11x11"), 'same' padding, on the default path (R*C > 128 takes the
+# implicit-GEMM kernel) and on SIMT; integer inputs bit-exact.
+BIG_FILTERS = [(2, 40, 140, 16, 16, 9, 9, 4), (1, 36, 150, 16, 16, 11, 11, 5), (1, 30, 133, 32, 24, 11, 11, 5)]
+
+
+@pytest.mark.parametrize("algo", [AUTO, SIMT])
+@pytest.mark.parametrize("shape", BIG_FILTERS)
+def test_conv_9x9_11x11_filters(algo, shape):
+    X, Wt, Y0, Y = _run(shape, algo)
+    R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, shape[-1])
+    assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL
+
+
+def test_conv_11x11_integer_bit_exact():
+    shape = (1, 24, 140, 16, 16, 11, 11, 5)
+    X, Wt, Y0, Y = _run(shape, AUTO, kind="integer")
+    R, _ = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, shape[-1])
+    assert np.array_equal(Y.astype(np.float64), R)
+
+
+def test_conv_paper_exact_valid_shape_sampled_pixels():
+    """PAPER.md:826 with valid padding: output 510x510,
+    the im2col GEMM M = 32*510*510 = 8,323,200, N = 16, K = 144."""
+    shape = (32, 512, 512, 16, 16, 3, 3, 0)
+    X, Wt, Y0, Y = _run(shape, AUTO, seed=1809)
+    P = Y.shape[0]
+    assert P == 32 * 510 * 510
+    g = si.rng(6)
+    pix = np.unique(np.concatenate([g.integers(0, P, 3000), [0, 509, 510, 510 * 509, P - 1, P - 510]]))
+    R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, 0, pixels=pix)
+    assert float(np.max(oracle.normalized_error(Y[pix], R, D))) <= TOL
+
+
+def test_conv_simt_fallback_accepts_wide_channels():
+    """C = 2576 with F % 4 != 0 misses the tensor-core rule; the SIMT fallback
+    tiles the channel dimension through shared memory, so AUTO accepts it."""
+    shape = (1, 6, 7, 2576, 18, 3, 3, 1)
+    X, Wt, Y0, Y = _run(shape, AUTO)
+    R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, 1)
+    assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL

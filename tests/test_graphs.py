@@ -1,8 +1,8 @@
 """CUDA-graph capture of the GEMM (streams and graphs instead of a tracing
-compiler): tm_sgemm enqueues only kernels and memsets, so a call captured once
-(after one warm-up call that sizes the library's stream-K workspace) replays
-correctly -- including stream-K schedules, whose per-launch epoch flags are
-cleared inside the graph before each replay (csrc/api.cpp streamk_workspace)."""
+compiler): tm_sgemm enqueues only kernels, memsets and (under capture) a
+graph-owned workspace allocation, so a captured call replays correctly --
+including stream-K schedules, whose epoch flags are cleared inside the graph
+before each replay (csrc/api.cpp streamk_workspace)."""
 import os
 
 import numpy as np
@@ -50,22 +50,46 @@ def test_captured_sgemm_replays(cfg):
         assert err <= TOL, (cfg, rep, err)
 
 
-def test_capture_without_workspace_is_an_error_not_a_hang():
-    """A stream-K launch whose workspace does not exist yet cannot allocate it
-    during capture: the call reports TM_ERR_INVALID_VALUE instead."""
+@pytest.mark.parametrize("cfg", ["2,64,1", "2,128,0"])
+def test_default_graph_idiom_and_replay_on_other_streams(cfg):
+    """The standard torch.cuda.graph idiom (warm-up on a side stream, capture on
+    torch's own capture stream, no stream argument): stream-K and wave-barrier
+    launches allocate their workspace inside the graph, so capture needs no
+    prior call on the capturing stream, and replays on other streams, two graphs
+    of the same shape, and direct calls in between do not share flags."""
     import torch
     import paper_1804_10694_b200 as tm
-    m, n, k = 1060, 1060, 1060
-    dA = torch.zeros((m, k), device="cuda")
-    dB = torch.zeros((k, n), device="cuda")
-    dC = torch.zeros((m, n), device="cuda")
-    s = torch.cuda.Stream()  # fresh stream: no workspace yet
-    os.environ["TM_TC_CONFIG"] = "2,64,1"
-    g = torch.cuda.CUDAGraph()
+    # 2,128,0 at 4096 x 4096 x 2048: 256 tiles on 74 clusters, 64 K-blocks -> wave barrier
+    m, n, k = (1060, 1060, 1060) if cfg == "2,64,1" else (4096, 4096, 2048)
+    A, B, _ = si.matrices(m, n, k, 43)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dC1 = torch.zeros((m, n), device="cuda")
+    dC2 = torch.zeros((m, n), device="cuda")
+    os.environ["TM_TC_CONFIG"] = cfg
     try:
-        with pytest.raises(tm.TmError):
-            with torch.cuda.graph(g, stream=s):
-                tm.sgemm_ex(dA, dB, dC, 1.0, 0.5, tm.ALGO_TF32X3)
+        graphs = []
+        for dC in (dC1, dC2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                tm.sgemm_ex(dA, dB, dC, si.ALPHA, si.BETA, tm.ALGO_TF32X3)
+            graphs.append(g)
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        for rep in range(2):
+            C0 = si.uniform(si.rng(300 + rep), (m, n))
+            dC1.copy_(torch.from_numpy(C0))
+            dC2.copy_(torch.from_numpy(C0))
+            torch.cuda.synchronize()
+            for g, s in zip(graphs, streams):
+                with torch.cuda.stream(s):
+                    g.replay()
+            dD = torch.from_numpy(C0).cuda()
+            tm.sgemm_ex(dA, dB, dD, si.ALPHA, si.BETA, tm.ALGO_TF32X3)  # direct call while graphs run
+            torch.cuda.synchronize()
+            rows = si.sample_rows(m, count=64)
+            R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0, rows=rows)
+            for out in (dC1, dC2, dD):
+                err = float(np.max(oracle.normalized_error(out.cpu().numpy()[rows], R, D)))
+                assert err <= TOL, (cfg, rep, err)
+            assert torch.equal(dC1, dC2) and torch.equal(dC1, dD)  # deterministic across paths
     finally:
         del os.environ["TM_TC_CONFIG"]
-    torch.cuda.synchronize()
