@@ -373,7 +373,7 @@ def main():
     value = flops * args.steps / (total_ms * 1e-3) / 1e9  # GFLOP/s, whole job
 
     # roofline of the dominant kernel (the GEMM), from this rank's live event times
-    kernel = path if path in ("simt", "tf32x1") else "tf32x3"
+    kernel = "simt" if path in ("simt", "simt_small") else path if path == "tf32x1" else "tf32x3"
     bound, peak, unit, peak_note = roofline_peak(kernel, peaks)
     my_flops = 2.0 * rows * n * k
     my_ms = statistics.median(per_step)  # the paper reports medians
@@ -389,7 +389,10 @@ def main():
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
             "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_unit": "bytes per launch",
             "traffic_source": traffic_src, "kernel": f"k_sgemm_tc ({path})" if kernel != "simt"
-            else "k_sgemm_simt", "peak_source": peak_note}
+            else ("k_sgemm_small" if path == "simt_small" else "k_sgemm_simt"), "peak_source": peak_note}
+    if path == "simt_small":
+        roof["note"] = ("launch-latency bound (SURVEY.md 8(d): C1's roofline fraction is not meaningful; "
+                        "step_ms.median is the figure)")
     if bound == "tensor":
         per_product = 1.0 if kernel == "tf32x1" else 3.0  # tensor MMAs per fp32 product
         sus = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / per_product

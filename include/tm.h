@@ -64,9 +64,14 @@ typedef enum {
 } tm_status;
 
 /* Path selection for tm_sgemm_ex.
- *  TM_ALGO_AUTO      3xTF32 tensor-core path when its layout rules hold
- *                    (A, B, C 16-byte aligned; lda, ldb, ldc multiples of 4),
- *                    else the SIMT path.  Misalignment is never an error here.
+ *  TM_ALGO_AUTO      problems of at most 2^22 multiply-adds (m*n*k) with
+ *                    k <= 256 take the small-GEMM kernel (FP32 FFMA, one CTA
+ *                    per 32x32 / 64x64 tile, launch-latency bound --
+ *                    BASELINE.json configs[0]);
+ *                    otherwise the 3xTF32 tensor-core path when its layout
+ *                    rules hold (A, B, C 16-byte aligned; lda, ldb, ldc
+ *                    multiples of 4), else the SIMT path.  Misalignment is
+ *                    never an error here.
  *  TM_ALGO_TF32X3    3xTF32 split-operand tcgen05 MMA (fp32 result, TMEM
  *                    accumulation).  Misaligned input -> TM_ERR_INVALID_VALUE.
  *  TM_ALGO_SIMT_F32  pure-FP32 FFMA register-blocked kernel (validation path).
@@ -194,7 +199,8 @@ tm_status tm_tune_cache_save(const char* path);
 int tm_tune_cache_load(const char* path);
 
 /* The plan tm_sgemm_op(opa, opb, ..., algo) would use (host-only, no launch):
- * *path = 0 invalid, 1 no-op, 2 scale, 3 tensor cores, 4 SIMT; for tensor
+ * *path = 0 invalid, 1 no-op, 2 scale, 3 tensor cores, 4 SIMT, 5 small-GEMM
+ * SIMT kernel; for tensor
  * cores the CTA group, CTA tile width and schedule (tuned entry if cached,
  * else the cost model).  Output pointers may be NULL.  Returns
  * TM_ERR_INVALID_VALUE for arguments the call would reject. */
@@ -203,7 +209,8 @@ tm_status tm_sgemm_plan_config(int opa, int opb, int64_t m, int64_t n, int64_t k
                                int algo, int* path, int* cg, int* bn_cta, int* streamk);
 
 /* Name of the path tm_sgemm_ex would take for these arguments on the current
- * device ("tf32x3", "simt", "scale", "noop", or "invalid"); host-only, no launch. */
+ * device ("tf32x3", "tf32x1", "simt", "simt_small", "scale", "noop", or
+ * "invalid"); host-only, no launch. */
 const char* tm_sgemm_plan_name(int64_t m, int64_t n, int64_t k, float alpha,
                                const float* A, int64_t lda, const float* B, int64_t ldb,
                                float beta, const float* C, int64_t ldc, int algo);

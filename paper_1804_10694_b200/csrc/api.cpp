@@ -66,7 +66,19 @@ int64_t extent_bytes(int64_t rows, int64_t cols, int64_t ld) {
   return ((rows - 1) * ld + cols) * 4;
 }
 
-enum class Path { kInvalid, kNoop, kScale, kTc, kSimt };
+enum class Path { kInvalid, kNoop, kScale, kTc, kSimt, kSmall };
+
+// AUTO sends problems of at most this many multiply-adds (m*n*k) and K <= 256
+// to the latency-bound small kernel (small_gemm.cu): there the tensor-core
+// kernel's fixed cost (cluster launch, TMEM, pipeline fill) dominates; beyond
+// (or for deeper K, whose 32-deep slices form one dependent chain per CTA) the
+// tensor cores win (measured crossover, scripts/r02/small_probe.py,
+// profiles/small_probe_r02.txt).  TM_SMALL_MAX overrides the size (tests/bench).
+int64_t small_max() {
+  const char* e = std::getenv("TM_SMALL_MAX");
+  return e ? std::atoll(e) : (1LL << 22);
+}
+constexpr int64_t kSmallMaxK = 256;
 
 struct Plan {
   Path path = Path::kInvalid;
@@ -111,6 +123,10 @@ Plan make_plan(const GemmArgs& a, int algo, int num_sms) {
       pl.path = Path::kTc;
       break;
     default:
+      if (a.m * a.n * a.k <= small_max() && a.k <= kSmallMaxK && small_fits(a.m, a.n, a.k)) {
+        pl.path = Path::kSmall;
+        return pl;
+      }
       pl.path = aligned ? Path::kTc : Path::kSimt;
   }
   if (pl.path == Path::kTc) {
@@ -154,11 +170,11 @@ tm_status run(const GemmArgs& a, int algo, cudaStream_t stream, int sm_reserve =
     explicit Range(const char* n) { nvtxRangePushA(n); }
     ~Range() { nvtxRangePop(); }
   } range(pl.path == Path::kTc ? (pl.tc.streamk ? "tm_sgemm tf32x3 stream-K" : "tm_sgemm tf32x3")
-                               : pl.path == Path::kSimt ? "tm_sgemm simt" : "tm_sgemm scale");
+          : pl.path == Path::kSimt ? "tm_sgemm simt" : pl.path == Path::kSmall ? "tm_sgemm simt small" : "tm_sgemm scale");
   if (log_enabled())
     std::fprintf(stderr, "[tm] sgemm m=%lld n=%lld k=%lld algo=%d -> %s cg=%d bn=%d split3=%d\n",
                  static_cast<long long>(a.m), static_cast<long long>(a.n), static_cast<long long>(a.k), algo,
-                 pl.path == Path::kTc ? "tf32x3" : pl.path == Path::kSimt ? "simt" : "scale", pl.tc.cg,
+                 pl.path == Path::kTc ? "tf32x3" : pl.path == Path::kSimt ? "simt" : pl.path == Path::kSmall ? "simt_small" : "scale", pl.tc.cg,
                  pl.tc.bn_cta, pl.tc.split3 ? 1 : 0);
   if (log_enabled() && pl.path == Path::kTc) std::fprintf(stderr, "[tm]   streamk=%d\n", pl.tc.streamk ? 1 : 0);
   switch (pl.path) {
@@ -166,6 +182,8 @@ tm_status run(const GemmArgs& a, int algo, cudaStream_t stream, int sm_reserve =
       return launch_scale(a.m, a.n, a.beta, a.C, a.ldc, stream);
     case Path::kSimt:
       return launch_simt(a, stream);
+    case Path::kSmall:
+      return launch_small(a, stream);
     case Path::kTc:
       return launch_tc(a, pl.tc, sms, stream);
     default:
@@ -432,6 +450,7 @@ const char* tm_sgemm_plan_name(int64_t m, int64_t n, int64_t k, float alpha, con
     case tmk::Path::kNoop: return "noop";
     case tmk::Path::kScale: return "scale";
     case tmk::Path::kSimt: return "simt";
+    case tmk::Path::kSmall: return "simt_small";
     case tmk::Path::kTc: return pl.tc.split3 ? "tf32x3" : "tf32x1";
     default: return "invalid";
   }

@@ -37,6 +37,11 @@ TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms) {
   TcChoice best = cands[0];
   double best_t = 1e300;
   const int64_t kb = (k + 31) / 32;
+  // Latency-bound one-wave problems (every 128 x 32 tile gets its own SM, short
+  // K): the narrowest 1-CTA tile, data-parallel, has the least per-CTA work
+  // between launch and epilogue -- the measured best from 128^3 to 768^3
+  // (scripts/r02/small_probe.py, profiles/small_probe_r02.txt).
+  if (((m + 127) / 128) * ((n + 31) / 32) <= num_sms && kb <= 32) return TcChoice{1, 32, true, false};
   for (const TcChoice& c : cands) {
     const int64_t tile_m = 128LL * c.cg, tile_n = static_cast<int64_t>(c.bn_cta) * c.cg;
     const int64_t tiles = ((m + tile_m - 1) / tile_m) * ((n + tile_n - 1) / tile_n);

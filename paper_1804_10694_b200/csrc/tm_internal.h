@@ -57,6 +57,10 @@ inline tm_status launch_tc(const GemmArgs& a, const TcChoice& c, int num_sms, cu
   return launch_tc_op<true, true>(a, c, num_sms, stream);
 }
 tm_status launch_simt(const GemmArgs& a, cudaStream_t stream);
+// Latency-bound small problems (small_gemm.cu): FP32 FFMA, one CTA per 32x32
+// or 64x64 tile.  small_fits: the index ranges it supports.
+bool small_fits(int64_t m, int64_t n, int64_t k);
+tm_status launch_small(const GemmArgs& a, cudaStream_t stream);
 tm_status launch_scale(int64_t m, int64_t n, float beta, float* C, int64_t ldc, cudaStream_t stream);
 // Reads `bytes` (a multiple of 16) of `buf` to evict L2 between timed runs (tune.cpp).
 tm_status launch_l2_flush(const float* buf, int64_t bytes, cudaStream_t stream);

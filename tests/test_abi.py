@@ -86,9 +86,14 @@ def test_no_cpu_fallback():
 
 def test_plan_dispatch_by_alignment():
     # aligned pointers + ld % 4 == 0 -> tensor cores; otherwise SIMT (never an error under AUTO)
-    assert tm.plan_name(64, 64, 64, 1.0, 0.0, 1 << 12, 64, 1 << 16, 64, 1 << 24, 64) == "tf32x3"
-    assert tm.plan_name(64, 64, 64, 1.0, 0.0, (1 << 12) + 4, 64, 1 << 16, 64, 1 << 24, 64) == "simt"
-    assert tm.plan_name(64, 63, 64, 1.0, 0.0, 1 << 12, 64, 1 << 16, 63, 1 << 24, 63) == "simt"
+    # small problems (m*n*k <= 2^22, k <= 256) take the latency-bound small kernel, aligned or not
+    assert tm.plan_name(64, 64, 64, 1.0, 0.0, 1 << 12, 64, 1 << 16, 64, 1 << 24, 64) == "simt_small"
+    assert tm.plan_name(64, 64, 64, 1.0, 0.0, (1 << 12) + 4, 64, 1 << 16, 64, 1 << 24, 64) == "simt_small"
+    assert tm.plan_name(128, 128, 256, 1.0, 0.0, 1 << 12, 256, 1 << 16, 128, 1 << 28, 128) == "simt_small"
+    assert tm.plan_name(64, 64, 260, 1.0, 0.0, 1 << 12, 260, 1 << 16, 64, 1 << 28, 64) == "tf32x3"  # deep K
+    assert tm.plan_name(256, 256, 260, 1.0, 0.0, 1 << 12, 260, 1 << 16, 256, 1 << 28, 256) == "tf32x3"
+    assert tm.plan_name(256, 255, 260, 1.0, 0.0, 1 << 12, 260, 1 << 16, 255, 1 << 28, 255) == "simt"
+    assert tm.plan_name(512, 64, 1024, 1.0, 0.0, (1 << 12) + 4, 1024, 1 << 16, 64, 1 << 28, 64) == "simt"
     assert tm.plan_name(64, 64, 64, 1.0, 0.0, 1 << 12, 64, 1 << 16, 64, 1 << 24, 64, algo=2) == "simt"
     assert tm.plan_name(64, 64, 64, 1.0, 0.0, 1 << 12, 64, 1 << 16, 64, 1 << 24, 64, algo=3) == "tf32x1"
     # special cases

@@ -245,7 +245,7 @@ def test_auto_offsets_and_views():
     the tensor-core path, misaligned ones fall back to SIMT; both correct."""
     import torch
     import paper_1804_10694_b200 as tm
-    m, n, k = 300, 200, 260
+    m, n, k = 600, 400, 520  # above the small-kernel threshold (m*n*k > 2^24)
     A, B, C0 = si.matrices(m + 4, n + 4, k + 4, seed=99)  # leading dims multiples of 4
     dA, dB, dC = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (A, B, C0))
     assert dA.stride(0) % 4 == 0 and dB.stride(0) % 4 == 0
