@@ -29,7 +29,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "sgemm GFLOP/s and % of TF32/FP32 roofline at 1/2/4/8 B200 vs CPU oracle"
-ALGOS = {"auto": 0, "tf32x3": 1, "simt": 2, "tf32x1": 3}
+ALGOS = {"auto": 0, "tf32x3": 1, "simt": 2, "tf32x1": 3, "bf16x9": 4}
 
 
 def load_peaks():
@@ -67,6 +67,8 @@ def roofline_peak(path, peaks):
     unit counts (148 SMs x 128 FP32 lanes x 2 flop x max SM clock)."""
     if path == "simt":
         return "alu", 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12, "TFLOP/s", "148 SM x 128 FFMA/clk x 2 x sm_max_mhz"
+    if path == "bf16x9":  # nine bf16 MMAs per fp32 product
+        return "tensor", peaks["bf16_tflops"] / 9.0, "TFLOP/s", f"{peaks['source']} bf16 {peaks['bf16_tflops']} / 9 (BF16x9)"
     tf32 = peaks["bf16_tflops"] * (1.1 / 2.25)
     if path == "tf32x1":  # one MMA per product: the TF32 dense peak itself
         return "tensor", tf32, "TFLOP/s", f"{peaks['source']} bf16 {peaks['bf16_tflops']} x 1.1/2.25 (tf32, 1xTF32)"
@@ -373,7 +375,7 @@ def main():
     value = flops * args.steps / (total_ms * 1e-3) / 1e9  # GFLOP/s, whole job
 
     # roofline of the dominant kernel (the GEMM), from this rank's live event times
-    kernel = "simt" if path in ("simt", "simt_small") else path if path == "tf32x1" else "tf32x3"
+    kernel = "simt" if path in ("simt", "simt_small") else path if path in ("tf32x1", "bf16x9") else "tf32x3"
     bound, peak, unit, peak_note = roofline_peak(kernel, peaks)
     my_flops = 2.0 * rows * n * k
     my_ms = statistics.median(per_step)  # the paper reports medians
@@ -394,14 +396,15 @@ def main():
         roof["note"] = ("launch-latency bound (SURVEY.md 8(d): C1's roofline fraction is not meaningful; "
                         "step_ms.median is the figure)")
     if bound == "tensor":
-        per_product = 1.0 if kernel == "tf32x1" else 3.0  # tensor MMAs per fp32 product
-        sus = peaks["bf16_tflops_sustained"] * (1.1 / 2.25) / per_product
+        per_product = {"tf32x1": 1.0, "bf16x9": 9.0}.get(kernel, 3.0)  # tensor MMAs per fp32 product
+        ratio = 1.0 if kernel == "bf16x9" else 1.1 / 2.25                  # bf16 -> tf32 nominal
+        sus = peaks["bf16_tflops_sustained"] * ratio / per_product
         roof["frac_of_sustained_peak"] = round(achieved / sus, 4)
         # clock-normalised: against the tf32 rate measured by scripts/mma_rate.py
-        # (4096 flop/clk/SM, kind::tf32) at the median SM clock sampled under load
+        # (4096 flop/clk/SM, kind::tf32; bf16 twice that) at the median SM clock sampled under load
         f_sm = clocks.summary().get("sm_mhz")
         if f_sm:
-            clk_peak = 148 * 4096 * f_sm * 1e6 / 1e12 / per_product
+            clk_peak = 148 * (8192 if kernel == "bf16x9" else 4096) * f_sm * 1e6 / 1e12 / per_product
             roof["frac_clock_normalized"] = round(achieved / clk_peak, 4)
             roof["clock_normalized_peak"] = round(clk_peak, 2)
     launches = args.steps * (1 if comm is None else max(1, min(8, k // 512)))
@@ -411,7 +414,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "step_ms": {"median": round(med_ms, 4), "min": round(min(per_step), 4), "max": round(max(per_step), 4)},
         "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": {"simt": "f32", "tf32x1": "tf32 (1xTF32 tensor-core, fp32 accumulate)"}.get(
+        "scaling": "strong", "vs_baseline": None, "dtype": {"simt": "f32", "tf32x1": "tf32 (1xTF32 tensor-core, fp32 accumulate)",
+                                                          "bf16x9": "f32 (BF16x9 tensor-core, fp32 accumulate)"}.get(
             kernel, "f32 (3xTF32 tensor-core, fp32 accumulate)"), "data": "synthetic (seeded U[-1,1) fp32, device-generated)",
         "config": {"workload": desc, "m": m, "n": n, "k": k, "alpha": alpha, "beta": beta, "path": path,
                    "rows_per_rank": rows, "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",

@@ -85,12 +85,28 @@ typedef enum {
  *                    2e-3; it does NOT meet the 1e-5 contract and AUTO never
  *                    selects it.  Integer inputs |x| <= 2048 are exact in TF32,
  *                    so their products are exact.  Same layout rules,
- *                    transposes and special cases as TF32X3. */
+ *                    transposes and special cases as TF32X3.
+ *  TM_ALGO_BF16X9    BF16x9 precision variant: every
+ *                    fp32 operand is split in the kernel into three bf16
+ *                    pieces x = b0 + b1 + b2 (b0 = RN_bf16(x), b1 =
+ *                    RN_bf16(x - b0), b2 = x - b0 - b1; exact for normal fp32:
+ *                    8 + 8 + 8 significant bits) and all nine products a_i b_j
+ *                    run on kind::f16 tcgen05 MMAs -- each product exact in
+ *                    fp32, so the only error is the fp32 accumulation (the
+ *                    3xTF32 path's scheme: round-toward-zero partials of K_c =
+ *                    128, RN promotion), about 1.5x as many roundings per K as
+ *                    TF32X3 and no representation error (TF32X3: 2^-19 per
+ *                    product).  Meets the 1e-5 contract (tests/test_bf16x9.py);
+ *                    integer inputs are bit-exact.  Runs at the bf16 tensor
+ *                    rate / 9 (TF32X3: tf32 rate / 3, about 1.5x faster), so
+ *                    AUTO never selects it.  Same layout rules, transposes and
+ *                    special cases as TF32X3. */
 typedef enum {
     TM_ALGO_AUTO = 0,
     TM_ALGO_TF32X3 = 1,
     TM_ALGO_SIMT_F32 = 2,
-    TM_ALGO_TF32X1 = 3
+    TM_ALGO_TF32X1 = 3,
+    TM_ALGO_BF16X9 = 4
 } tm_algo;
 
 /* C = alpha*A*B + beta*C on `stream`.  A: m x k (lda),

@@ -14,12 +14,12 @@ import ctypes
 import os
 
 __all__ = [
-    "ALGO_AUTO", "ALGO_TF32X3", "ALGO_SIMT_F32", "ALGO_TF32X1", "TmError", "lib", "lib_path", "sgemm",
+    "ALGO_AUTO", "ALGO_TF32X3", "ALGO_SIMT_F32", "ALGO_TF32X1", "ALGO_BF16X9", "TmError", "lib", "lib_path", "sgemm",
     "sgemm_ex", "sgemm_host", "plan_name", "plan_config", "tune", "tune_cache_save", "tune_cache_load",
     "tune_cache_clear", "tune_cache_size", "dist_rows", "Comm", "status_string", "EXPORTED_SYMBOLS",
 ]
 
-ALGO_AUTO, ALGO_TF32X3, ALGO_SIMT_F32, ALGO_TF32X1 = 0, 1, 2, 3
+ALGO_AUTO, ALGO_TF32X3, ALGO_SIMT_F32, ALGO_TF32X1, ALGO_BF16X9 = 0, 1, 2, 3, 4
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_PKG, "_lib", "libtm.so")

@@ -82,7 +82,7 @@ constexpr int64_t kSmallMaxK = 256;
 
 struct Plan {
   Path path = Path::kInvalid;
-  TcChoice tc{2, 128, true, false};
+  TcChoice tc{2, 128, 1, false};
 };
 
 bool tc_aligned(const GemmArgs& a) {
@@ -94,7 +94,7 @@ bool tc_aligned(const GemmArgs& a) {
 Plan make_plan(const GemmArgs& a, int algo, int num_sms) {
   Plan pl;
   if (a.m < 0 || a.n < 0 || a.k < 0) return pl;
-  if (algo < TM_ALGO_AUTO || algo > TM_ALGO_TF32X1) return pl;
+  if (algo < TM_ALGO_AUTO || algo > TM_ALGO_BF16X9) return pl;
   if (a.m == 0 || a.n == 0) {
     pl.path = Path::kNoop;
     return pl;
@@ -119,6 +119,7 @@ Plan make_plan(const GemmArgs& a, int algo, int num_sms) {
       break;
     case TM_ALGO_TF32X3:
     case TM_ALGO_TF32X1:
+    case TM_ALGO_BF16X9:
       if (!aligned) return pl;
       pl.path = Path::kTc;
       break;
@@ -131,9 +132,9 @@ Plan make_plan(const GemmArgs& a, int algo, int num_sms) {
   }
   if (pl.path == Path::kTc) {
     pl.tc = plan_tc(a.m, a.n, a.k, num_sms > 0 ? num_sms : 148);
-    pl.tc.split3 = (algo != TM_ALGO_TF32X1);
+    pl.tc.prec = algo == TM_ALGO_TF32X1 ? 0 : algo == TM_ALGO_BF16X9 ? 2 : 1;  // tc_gemm.cuh kPrec*
     TcChoice tuned;
-    if (pl.tc.split3 && tune_lookup(a, num_sms > 0 ? num_sms : 148, &tuned)) {  // measured choice (tune.cpp)
+    if (pl.tc.prec == 1 && tune_lookup(a, num_sms > 0 ? num_sms : 148, &tuned)) {  // measured choice (tune.cpp)
       pl.tc.cg = tuned.cg;
       pl.tc.bn_cta = tuned.bn_cta;
       pl.tc.streamk = tuned.streamk;
@@ -172,10 +173,10 @@ tm_status run(const GemmArgs& a, int algo, cudaStream_t stream, int sm_reserve =
   } range(pl.path == Path::kTc ? (pl.tc.streamk ? "tm_sgemm tf32x3 stream-K" : "tm_sgemm tf32x3")
           : pl.path == Path::kSimt ? "tm_sgemm simt" : pl.path == Path::kSmall ? "tm_sgemm simt small" : "tm_sgemm scale");
   if (log_enabled())
-    std::fprintf(stderr, "[tm] sgemm m=%lld n=%lld k=%lld algo=%d -> %s cg=%d bn=%d split3=%d\n",
+    std::fprintf(stderr, "[tm] sgemm m=%lld n=%lld k=%lld algo=%d -> %s cg=%d bn=%d prec=%d\n",
                  static_cast<long long>(a.m), static_cast<long long>(a.n), static_cast<long long>(a.k), algo,
                  pl.path == Path::kTc ? "tf32x3" : pl.path == Path::kSimt ? "simt" : pl.path == Path::kSmall ? "simt_small" : "scale", pl.tc.cg,
-                 pl.tc.bn_cta, pl.tc.split3 ? 1 : 0);
+                 pl.tc.bn_cta, pl.tc.prec);
   if (log_enabled() && pl.path == Path::kTc) std::fprintf(stderr, "[tm]   streamk=%d\n", pl.tc.streamk ? 1 : 0);
   switch (pl.path) {
     case Path::kScale:
@@ -451,7 +452,7 @@ const char* tm_sgemm_plan_name(int64_t m, int64_t n, int64_t k, float alpha, con
     case tmk::Path::kScale: return "scale";
     case tmk::Path::kSimt: return "simt";
     case tmk::Path::kSmall: return "simt_small";
-    case tmk::Path::kTc: return pl.tc.split3 ? "tf32x3" : "tf32x1";
+    case tmk::Path::kTc: return pl.tc.prec == 1 ? "tf32x3" : pl.tc.prec == 0 ? "tf32x1" : "bf16x9";
     default: return "invalid";
   }
 }
@@ -480,7 +481,8 @@ tm_status tm_sgemm_host(int64_t m, int64_t n, int64_t k, float alpha, const floa
                         int algo) {
   try {
     GemmArgs chk{m, n, k, alpha, beta, A_host, lda, B_host, ldb, C_host, ldc};
-    tmk::Plan pre = tmk::make_plan(chk, algo == TM_ALGO_TF32X3 || algo == TM_ALGO_TF32X1 ? TM_ALGO_SIMT_F32 : algo, 148);
+    tmk::Plan pre = tmk::make_plan(chk, algo == TM_ALGO_TF32X3 || algo == TM_ALGO_TF32X1 || algo == TM_ALGO_BF16X9
+                                            ? TM_ALGO_SIMT_F32 : algo, 148);
     if (pre.path == tmk::Path::kInvalid) return TM_ERR_INVALID_VALUE;
     if (pre.path == tmk::Path::kNoop) return TM_OK;
     tmk::DevInfo* dev = nullptr;

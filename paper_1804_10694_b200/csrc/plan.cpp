@@ -32,8 +32,8 @@ bool plan_streamk(int64_t m, int64_t n, int64_t k, int cg, int bn_cta, int num_s
 }
 
 TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms) {
-  static const TcChoice cands[] = {{2, 128, true, false}, {2, 64, true, false}, {2, 32, true, false},
-                                   {1, 128, true, false}, {1, 64, true, false}, {1, 32, true, false}};
+  static const TcChoice cands[] = {{2, 128, 1, false}, {2, 64, 1, false}, {2, 32, 1, false},
+                                   {1, 128, 1, false}, {1, 64, 1, false}, {1, 32, 1, false}};
   TcChoice best = cands[0];
   double best_t = 1e300;
   const int64_t kb = (k + 31) / 32;
@@ -41,7 +41,7 @@ TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms) {
   // K): the narrowest 1-CTA tile, data-parallel, has the least per-CTA work
   // between launch and epilogue -- the measured best from 128^3 to 768^3
   // (scripts/r02/small_probe.py, profiles/small_probe_r02.txt).
-  if (((m + 127) / 128) * ((n + 31) / 32) <= num_sms && kb <= 32) return TcChoice{1, 32, true, false};
+  if (((m + 127) / 128) * ((n + 31) / 32) <= num_sms && kb <= 32) return TcChoice{1, 32, 1, false};
   for (const TcChoice& c : cands) {
     const int64_t tile_m = 128LL * c.cg, tile_n = static_cast<int64_t>(c.bn_cta) * c.cg;
     const int64_t tiles = ((m + tile_m - 1) / tile_m) * ((n + tile_n - 1) / tile_n);

@@ -243,6 +243,31 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint6
 }
 #undef TM_MMA_TF32
 
+// D[tmem] (+)= A[smem] * B[smem], kind::f16 with bf16 operands, fp32 accumulate
+// (BF16x9 precision variant).  COLL: 0 discard, 1 fill, 2 lastuse, 3 use (keep
+// the collected A for a further MMA).
+#define TM_MMA_BF16(CGS, COLLS)                                                                        \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                                   \
+               "tcgen05.mma.cta_group::" CGS ".kind::f16" COLLS " [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem), \
+               "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)                                   \
+               : "memory")
+template <int CG, int COLL = 0>
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  if constexpr (CG == 1) {
+    if constexpr (COLL == 1) TM_MMA_BF16("1", ".collector::a::fill");
+    else if constexpr (COLL == 2) TM_MMA_BF16("1", ".collector::a::lastuse");
+    else if constexpr (COLL == 3) TM_MMA_BF16("1", ".collector::a::use");
+    else TM_MMA_BF16("1", "");
+  } else {
+    if constexpr (COLL == 1) TM_MMA_BF16("2", ".collector::a::fill");
+    else if constexpr (COLL == 2) TM_MMA_BF16("2", ".collector::a::lastuse");
+    else if constexpr (COLL == 3) TM_MMA_BF16("2", ".collector::a::use");
+    else TM_MMA_BF16("2", "");
+  }
+}
+#undef TM_MMA_BF16
+
 // D[tmem] (+)= A[tmem] * B[smem], kind::tf32 (A from tensor memory: 128 lanes =
 // rows, 32-bit columns = K, i.e. K-major).
 template <int CG>
@@ -350,6 +375,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, ui
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn_major, int b_mn_major) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn_major) << 15) |
          (static_cast<uint32_t>(b_mn_major) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Instruction descriptor, kind::f16, D = F32, A = B = BF16 (format code 1),
+// both operands K-major; same field positions as idesc_tf32.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 

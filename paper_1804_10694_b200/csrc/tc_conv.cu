@@ -54,7 +54,7 @@ bool encode_im2col(CUtensorMap* map, const ConvArgs& a, int bk, CUtensorMapSwizz
 
 template <int CG, int BN_CTA, int BK>
 tm_status launch_conv_cfg(const ConvArgs& a, bool streamk, int num_sms, cudaStream_t stream) {
-  using Cfg = TcCfg<CG, BN_CTA, true, BK>;
+  using Cfg = TcCfg<CG, BN_CTA, kPrecTf32x3, BK>;
   const CUtensorMapSwizzle swz = BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   CUtensorMap tmA, tmB;
   if (!encode_im2col(&tmA, a, BK, swz)) return TM_ERR_INTERNAL;
@@ -80,7 +80,7 @@ tm_status launch_conv_cfg(const ConvArgs& a, bool streamk, int num_sms, cudaStre
   p.cv_s = static_cast<int>(a.s);
   p.cv_c = static_cast<int>(a.c);
   p.cv_pad = static_cast<int>(a.pad);
-  return launch_kernel<CG, BN_CTA, true, false, true, BK, true>(tmA, tmB, p, num_sms, streamk, stream);
+  return launch_kernel<CG, BN_CTA, kPrecTf32x3, false, true, BK, true>(tmA, tmB, p, num_sms, streamk, stream);
 }
 
 }  // namespace

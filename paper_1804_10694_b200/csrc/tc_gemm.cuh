@@ -60,17 +60,32 @@ constexpr int kEpiStride = 20;     // floats per staged row (16 data + 4 pad: 16
 constexpr int kKcBlocksDefault = 4;   // K_c = 4 * 32 = 128: RZ partial length before RN promotion
 constexpr int kGroupMDefault = 16;    // raster: tile-rows per group (L2 reuse)
 
+// Precision variants of the tensor-core path (template parameter PREC):
+//   kPrecTf32x1  one kind::tf32 MMA per K step on the raw operands (fast, ~2e-3);
+//   kPrecTf32x3  x = hi + lo split, A_lo B_hi + A_hi B_lo + A_hi B_hi (the default);
+//   kPrecBf16x9  x = b0 + b1 + b2, three bf16 pieces that represent every fp32
+//                exactly (8 + 8 + 8 significant bits), all nine products
+//                sum_ij a_i b_j on kind::f16 MMAs (each product exact in fp32).
+constexpr int kPrecTf32x1 = 0, kPrecTf32x3 = 1, kPrecBf16x9 = 2;
+
 // Stage ring sizes from a shared-memory budget.  With A_lo in TMEM (kAlo: K-major
 // A and room for at least two A_lo stages beyond the two partial accumulators)
 // the lo ring holds only B_lo in shared memory and A_lo in TMEM columns, so it
 // is made as deep as TMEM allows (<= 8; also 8 for 1xTF32): for skinny tiles a stage carries only
 // a few short MMAs, and a 2-deep split -> MMA -> commit round trip would bound
 // the rate.  Otherwise two lo stages; as many raw (TMA) stages as fit, <= 12.
-template <int CG, int BN_CTA, bool SPLIT3, int BK = 32, bool TA = false>
+// BF16x9: the "lo" ring holds the split stage -- three bf16 planes of A (128
+// rows) and of B (BN_CTA rows), each K-major with 64-byte rows (32 k).
+template <int CG, int BN_CTA, int PREC, int BK = 32, bool TA = false>
 struct TcCfg {
+  static constexpr bool SPLIT3 = PREC == kPrecTf32x3;
+  static constexpr bool BF16 = PREC == kPrecBf16x9;
   static constexpr int kABytes = kBMCta * BK * 4;    // 16 KiB (BK 32) / 8 KiB (BK 16)
   static constexpr int kBBytes = BK * BN_CTA * 4;
   static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kPlaneA = kBMCta * BK * 2;    // one bf16 plane of A (BF16x9)
+  static constexpr int kPlaneB = BN_CTA * BK * 2;
+  static constexpr int kSplitStage = 3 * (kPlaneA + kPlaneB);
   static constexpr int kMmaM = kBMCta * CG;
   static constexpr int kMmaN = BN_CTA * CG;
   static constexpr bool kAlo = SPLIT3 && !TA && (2 * kMmaN + 2 * BK <= 512);
@@ -78,8 +93,8 @@ struct TcCfg {
   static constexpr int kLoTmem0 = kAlo ? (512 - 2 * kMmaN) / BK : 2;
   static constexpr int kLoTmem = kLoTmem0 < kLoFit ? kLoTmem0 : (kLoFit < 2 ? 2 : kLoFit);
   // ready/empty_lo ring depth (only pacing barriers, no storage, for 1xTF32)
-  static constexpr int kLo = !SPLIT3 ? 8 : kAlo ? (kLoTmem < 8 ? kLoTmem : 8) : 2;
-  static constexpr int kLoBytes = SPLIT3 ? kLo * (kAlo ? kBBytes : kStage) : 0;
+  static constexpr int kLo = PREC == kPrecTf32x1 ? 8 : kAlo ? (kLoTmem < 8 ? kLoTmem : 8) : 2;
+  static constexpr int kLoBytes = BF16 ? kLo * kSplitStage : SPLIT3 ? kLo * (kAlo ? kBBytes : kStage) : 0;
   static constexpr int kRawFit = (200 * 1024 - kLoBytes) / kStage;
   static constexpr int kRaw = kRawFit < 12 ? kRawFit : 12;
   static constexpr int kTileM = kMmaM;
@@ -90,6 +105,8 @@ struct TcCfg {
   static constexpr int kEpiStageBytes = kEpiWarps * 32 * kEpiStride * 4;  // transpose staging
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kRawBytes + kLoBytes + kEpiStageBytes + kNumBars * 8 + 16;
   static_assert(kRaw >= 3, "ring too shallow");
+  static_assert(!BF16 || BK == 32, "BF16x9: 32-k stages");
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 };
 
 struct TcParams {
@@ -164,6 +181,67 @@ __device__ __forceinline__ void split_tile(uint32_t src, uint32_t dst, int st) {
       const int idx = (b + i) * kSplitThreads + st;
       if (!kRagged || idx < kChunks) ptx::sts128(dst + idx * 16, tf32_lo4(v[i]));
     }
+  }
+}
+
+// ---- BF16x9 split (kPrecBf16x9) ----
+// x = b0 + b1 + b2 exactly: b0 = RN_bf16(x), b1 = RN_bf16(x - b0),
+// b2 = RN_bf16(x - b0 - b1); both subtractions are exact in fp32 and the last
+// remainder has at most 8 significant bits, so b2 is exact too (normal range).
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {  // lo -> bits 0..15
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ void split8_bf16(const float (&x)[8], uint4& p0, uint4& p1, uint4& p2) {
+  uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float a = x[2 * j], b = x[2 * j + 1];
+    w0[j] = pack_bf16x2(a, b);
+    const float ra = __fsub_rn(a, bf16_lo(w0[j])), rb = __fsub_rn(b, bf16_hi(w0[j]));
+    w1[j] = pack_bf16x2(ra, rb);
+    w2[j] = pack_bf16x2(__fsub_rn(ra, bf16_lo(w1[j])), __fsub_rn(rb, bf16_hi(w1[j])));
+  }
+  p0 = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+  p1 = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+  p2 = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+}
+// Row r of a raw fp32 stage -> the three bf16 planes of the split stage.
+//   KMAJOR_SRC: the raw tile is K-major, TMA SWIZZLE_128B (row r = 128 B of 32 k,
+//               16-B chunk c at c ^ (r % 8));
+//   else        MN-major without swizzle, rows of `ld_src` floats per k
+//               (element (k, r) at (k * ld_src + r) * 4).
+// Each plane is K-major with 64-B rows (32 bf16), SWIZZLE_64B: row r at
+// (r / 8) * 512 + (r % 8) * 64, 16-B chunk q at q ^ ((r / 2) % 4).
+template <bool KMAJOR_SRC>
+__device__ __forceinline__ void split_row_bf16(uint32_t src, int ld_src, int r, uint32_t plane0, uint32_t plane_bytes) {
+  const uint32_t drow = plane0 + (r >> 3) * 512 + (r & 7) * 64;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // k in [8q, 8q + 8)
+    float x[8];
+    if constexpr (KMAJOR_SRC) {
+      const uint32_t row = src + r * 128;
+      const uint4 v0 = ptx::lds128(row + (((2 * q) ^ (r & 7)) << 4));
+      const uint4 v1 = ptx::lds128(row + (((2 * q + 1) ^ (r & 7)) << 4));
+      x[0] = __uint_as_float(v0.x); x[1] = __uint_as_float(v0.y); x[2] = __uint_as_float(v0.z); x[3] = __uint_as_float(v0.w);
+      x[4] = __uint_as_float(v1.x); x[5] = __uint_as_float(v1.y); x[6] = __uint_as_float(v1.z); x[7] = __uint_as_float(v1.w);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint32_t w;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w) : "r"(src + ((8 * q + j) * ld_src + r) * 4));
+        x[j] = __uint_as_float(w);
+      }
+    }
+    uint4 p0, p1, p2;
+    split8_bf16(x, p0, p1, p2);
+    const uint32_t off = drow + ((q ^ ((r >> 1) & 3)) << 4);
+    ptx::sts128(off, p0);
+    ptx::sts128(off + plane_bytes, p1);
+    ptx::sts128(off + 2 * plane_bytes, p2);
   }
 }
 
@@ -388,10 +466,13 @@ __device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, 
 // rows, SWIZZLE_64B; K-major operands only).
 // CONV: A is the implicit im2col matrix of an NHWC activation tensor, loaded
 // with TMA im2col-mode copies (one filter tap x BK channels per stage).
-template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB, int BK = 32, bool CONV = false>
+template <int CG, int BN_CTA, int PREC, bool TA, bool TB, int BK = 32, bool CONV = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
-  using Cfg = TcCfg<CG, BN_CTA, SPLIT3, BK, TA>;
+  using Cfg = TcCfg<CG, BN_CTA, PREC, BK, TA>;
+  constexpr bool SPLIT3 = Cfg::SPLIT3;  // 3xTF32
+  constexpr bool BF16 = Cfg::BF16;      // BF16x9
+  static_assert(!BF16 || !CONV, "BF16x9: GEMM only");
   static_assert(BK == 32 || BK == 16, "BK");
   static_assert(BK == 32 || (!TA && TB), "64-B rows only for K-major operands");
   static_assert(TB || BN_CTA % 32 == 0, "MN-major B needs 32-column atoms");
@@ -519,12 +600,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         static_cast<uint16_t>(kx), static_cast<uint16_t>(ky));
               } else if constexpr (!TA) {  // A: one K-major box BK (k) x 128 (rows)
                 ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], kb * BK, row0);
+              } else if constexpr (BF16) {  // A^T: one un-swizzled box 128 (rows) x 32 (k)
+                ptx::tma_load_2d(rawA + s * Cfg::kABytes, &tmA, &full[s], row0, kb * BK);
               } else {              // A^T: four MN-major boxes 32 (rows) x 32 (k)
 #pragma unroll
                 for (int j = 0; j < kBMCta / 32; ++j)
                   ptx::tma_load_2d(rawA + s * Cfg::kABytes + j * 4096, &tmA, &full[s], row0 + 32 * j, kb * BK);
               }
-              if constexpr (!TB) {  // B: BN_CTA/32 MN-major boxes 32 (cols) x 32 (k)
+              if constexpr (!TB && BF16) {  // B: one un-swizzled box BN_CTA (cols) x 32 (k)
+                ptx::tma_load_2d(rawB + s * Cfg::kBBytes, &tmB, &full[s], col0, kb * BK);
+              } else if constexpr (!TB) {  // B: BN_CTA/32 MN-major boxes 32 (cols) x 32 (k)
 #pragma unroll
                 for (int j = 0; j < BN_CTA / 32; ++j)
                   ptx::tma_load_2d(rawB + s * Cfg::kBBytes + j * 4096, &tmB, &full[s], col0 + 32 * j, kb * BK);
@@ -574,6 +659,29 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::mbar_wait_cluster(&ready[sl], phl);
               ptx::tc_fence_after();
               if (first_mma) { trace_mark(p, 4); first_mma = false; }  // first MMA issue
+              if constexpr (BF16) {
+                // all nine products a_i * b_j per K = 16 step, smallest first; the
+                // three MMAs sharing A plane i read it from shared memory once
+                // (collector fill / use / lastuse)
+                constexpr uint32_t idesc_b = ptx::idesc_bf16(Cfg::kMmaM, Cfg::kMmaN);
+                const uint32_t st0 = loA_s + sl * Cfg::kSplitStage;
+#pragma unroll
+                for (int ks = 0; ks < BK / 16; ++ks) {
+#pragma unroll
+                  for (int ia = 2; ia >= 0; --ia) {
+                    const uint64_t aD = ptx::sdesc(st0 + ia * Cfg::kPlaneA + ks * 32, 16, 512, ptx::kLayoutSW64);
+#pragma unroll
+                    for (int ib = 2; ib >= 0; --ib) {
+                      const uint64_t bD = ptx::sdesc(st0 + 3 * Cfg::kPlaneA + ib * Cfg::kPlaneB + ks * 32, 16, 512,
+                                                     ptx::kLayoutSW64);
+                      const uint32_t acc = (kb != kb0 || ks != 0 || ia != 2 || ib != 2) ? 1u : 0u;
+                      if (ib == 2) ptx::mma_bf16<CG, 1>(d, aD, bD, idesc_b, acc);
+                      else if (ib == 1) ptx::mma_bf16<CG, 3>(d, aD, bD, idesc_b, acc);
+                      else ptx::mma_bf16<CG, 2>(d, aD, bD, idesc_b, acc);
+                    }
+                  }
+                }
+              } else {
 #pragma unroll
               for (int ks = 0; ks < BK / 8; ++ks) {
                 const uint64_t aH = TA ? desc_mn(rawA_s + s * Cfg::kABytes, ks) : desc_k(rawA_s + s * Cfg::kABytes, ks);
@@ -595,6 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                   ptx::mma_tf32<CG>(d, aH, bH, idesc, acc);
                 }
+              }
               }
               ptx::mma_commit<CG>(&empty_raw[s]);
               ptx::mma_commit<CG>(&empty_lo[sl]);  // also paces the ready ring when !SPLIT3
@@ -655,6 +764,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             split_tile<Cfg::kABytes>(rawA_s + s * Cfg::kABytes, loA_s + sl * Cfg::kABytes, st);
           }
           split_tile<Cfg::kBBytes>(rawB_s + s * Cfg::kBBytes, loB_s + sl * Cfg::kBBytes, st);
+          ptx::fence_proxy_async_smem();
+        } else if constexpr (BF16) {
+          // thread st splits row st of A (128 rows) and, if st < BN_CTA, row st of
+          // B^T (B column st) into the three K-major bf16 planes of split slot sl
+          const uint32_t dst = loA_s + sl * Cfg::kSplitStage;
+          split_row_bf16<!TA>(rawA_s + s * Cfg::kABytes, kBMCta, st, dst, Cfg::kPlaneA);
+          if (st < BN_CTA)
+            split_row_bf16<TB>(rawB_s + s * Cfg::kBBytes, BN_CTA, st, dst + 3 * Cfg::kPlaneA, Cfg::kPlaneB);
           ptx::fence_proxy_async_smem();
         }
         __syncwarp();
@@ -822,11 +939,11 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, 
 // Common launch: p carries the problem (m, n, k, tiles, kblocks, C, alpha,
 // beta, and the conv geometry for CONV kernels); this fills the schedule
 // (stream-K / wave barrier / tuning knobs) and launches the cluster kernel.
-template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB, int BK, bool CONV>
+template <int CG, int BN_CTA, int PREC, bool TA, bool TB, int BK, bool CONV>
 tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams p, int num_sms, bool streamk,
                         cudaStream_t stream) {
-  using Cfg = TcCfg<CG, BN_CTA, SPLIT3, BK, TA>;
-  auto kern = k_sgemm_tc<CG, BN_CTA, SPLIT3, TA, TB, BK, CONV>;
+  using Cfg = TcCfg<CG, BN_CTA, PREC, BK, TA>;
+  auto kern = k_sgemm_tc<CG, BN_CTA, PREC, TA, TB, BK, CONV>;
   static std::atomic<unsigned long long> optin{0};  // per instantiation, bit per device
   if (tm_status st = ensure_smem_optin(optin, kern, Cfg::kSmemBytes); st != TM_OK) return st;
   // Tuning knobs (bench/tests only), read once per process.
@@ -916,17 +1033,22 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
   return TM_OK;
 }
 
-template <int CG, int BN_CTA, bool SPLIT3, bool TA, bool TB>
+template <int CG, int BN_CTA, int PREC, bool TA, bool TB>
 tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t stream) {
-  using Cfg = TcCfg<CG, BN_CTA, SPLIT3>;
+  using Cfg = TcCfg<CG, BN_CTA, PREC>;
   CUtensorMap tmA, tmB;
   // K-major operands (A, B^T): box 32 (k) x rows, SWIZZLE_128B.  MN-major
-  // operands (A^T, B): box 32 (m or n) x 32 (k), 128-B swizzle with 32-B atoms.
+  // operands (A^T, B): box 32 (m or n) x 32 (k), 128-B swizzle with 32-B atoms
+  // for the tf32 MMAs; BF16x9 reads MN-major raw tiles only in its split
+  // warps, so it loads them as one un-swizzled box (128 or BN_CTA) x 32 (k).
+  constexpr bool BF16 = PREC == kPrecBf16x9;
   bool ok;
   if constexpr (!TA) ok = encode_2d(&tmA, a.A, a.m, a.k, a.lda, kBK, kBMCta, CU_TENSOR_MAP_SWIZZLE_128B);
+  else if constexpr (BF16) ok = encode_2d(&tmA, a.A, a.k, a.m, a.lda, kBMCta, kBK, CU_TENSOR_MAP_SWIZZLE_NONE);
   else ok = encode_2d(&tmA, a.A, a.k, a.m, a.lda, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok) return TM_ERR_INTERNAL;
-  if constexpr (!TB) ok = encode_2d(&tmB, a.B, a.k, a.n, a.ldb, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if constexpr (!TB && BF16) ok = encode_2d(&tmB, a.B, a.k, a.n, a.ldb, BN_CTA, kBK, CU_TENSOR_MAP_SWIZZLE_NONE);
+  else if constexpr (!TB) ok = encode_2d(&tmB, a.B, a.k, a.n, a.ldb, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   else ok = encode_2d(&tmB, a.B, a.n, a.k, a.ldb, kBK, BN_CTA, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!ok) return TM_ERR_INTERNAL;
   TcParams p{};
@@ -943,33 +1065,47 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t 
   p.beta = a.beta;
   p.C = a.C;
   p.ldc = a.ldc;
-  return launch_kernel<CG, BN_CTA, SPLIT3, TA, TB, 32, false>(tmA, tmB, p, num_sms, streamk, stream);
+  return launch_kernel<CG, BN_CTA, PREC, TA, TB, 32, false>(tmA, tmB, p, num_sms, streamk, stream);
 }
 
-template <bool SPLIT3, bool TA, bool TB>
+template <int PREC, bool TA, bool TB>
 tm_status launch_split(const GemmArgs& a, int cg, int bn, int num_sms, bool sk, cudaStream_t s) {
-  if (cg == 2) {
-    if (bn == 128) return launch_cfg<2, 128, SPLIT3, TA, TB>(a, num_sms, sk, s);
-    if (bn == 64) return launch_cfg<2, 64, SPLIT3, TA, TB>(a, num_sms, sk, s);
-    if (bn == 32) return launch_cfg<2, 32, SPLIT3, TA, TB>(a, num_sms, sk, s);
-  } else if (cg == 1) {
-    if (bn == 128) return launch_cfg<1, 128, SPLIT3, TA, TB>(a, num_sms, sk, s);
-    if (bn == 64) return launch_cfg<1, 64, SPLIT3, TA, TB>(a, num_sms, sk, s);
-    if (bn == 32) return launch_cfg<1, 32, SPLIT3, TA, TB>(a, num_sms, sk, s);
+  if constexpr (PREC == kPrecBf16x9) {
+    // BF16x9 is compiled for 64- and 128-column CTA tiles (32 -> 64)
+    if (bn == 32) bn = 64;
+    if (cg == 2 && bn == 128) return launch_cfg<2, 128, PREC, TA, TB>(a, num_sms, sk, s);
+    if (cg == 2 && bn == 64) return launch_cfg<2, 64, PREC, TA, TB>(a, num_sms, sk, s);
+    if (cg == 1 && bn == 128) return launch_cfg<1, 128, PREC, TA, TB>(a, num_sms, sk, s);
+    if (cg == 1 && bn == 64) return launch_cfg<1, 64, PREC, TA, TB>(a, num_sms, sk, s);
+    return TM_ERR_INVALID_VALUE;
+  } else {
+    if (cg == 2) {
+      if (bn == 128) return launch_cfg<2, 128, PREC, TA, TB>(a, num_sms, sk, s);
+      if (bn == 64) return launch_cfg<2, 64, PREC, TA, TB>(a, num_sms, sk, s);
+      if (bn == 32) return launch_cfg<2, 32, PREC, TA, TB>(a, num_sms, sk, s);
+    } else if (cg == 1) {
+      if (bn == 128) return launch_cfg<1, 128, PREC, TA, TB>(a, num_sms, sk, s);
+      if (bn == 64) return launch_cfg<1, 64, PREC, TA, TB>(a, num_sms, sk, s);
+      if (bn == 32) return launch_cfg<1, 32, PREC, TA, TB>(a, num_sms, sk, s);
+    }
+    return TM_ERR_INVALID_VALUE;
   }
-  return TM_ERR_INVALID_VALUE;
 }
 
 }  // namespace
 
 // Tensor-core launch for one operand layout (explicitly instantiated in
-// tc_gemm_{nn,nt,tn,tt}.cu): 3xTF32 (split3) or the single-pass 1xTF32
-// precision variant (one MMA per K step on the raw operands).
+// tc_gemm_{nn,nt,tn,tt}.cu): 3xTF32, the single-pass 1xTF32 precision variant
+// (one MMA per K step on the raw operands) or BF16x9.
 template <bool TA, bool TB>
 tm_status launch_tc_op(const GemmArgs& a, const TcChoice& c, int num_sms, cudaStream_t stream) {
   if (a.m > INT32_MAX / 2 || a.n > INT32_MAX / 2 || a.k > INT32_MAX / 2) return TM_ERR_INVALID_VALUE;
-  if (c.split3) return launch_split<true, TA, TB>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
-  return launch_split<false, TA, TB>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
+  switch (c.prec) {
+    case kPrecTf32x3: return launch_split<kPrecTf32x3, TA, TB>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
+    case kPrecTf32x1: return launch_split<kPrecTf32x1, TA, TB>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
+    case kPrecBf16x9: return launch_split<kPrecBf16x9, TA, TB>(a, c.cg, c.bn_cta, num_sms, c.streamk, stream);
+    default: return TM_ERR_INVALID_VALUE;
+  }
 }
 
 }  // namespace tmk

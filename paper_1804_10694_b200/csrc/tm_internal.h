@@ -40,11 +40,11 @@ struct GemmArgs {
 };
 
 // Tensor-core configuration: CTA group (1 or 2), B columns per CTA (32/64/128),
-// 3xTF32 (true) or single-pass TF32 (false, bring-up only).
+// precision variant (tc_gemm.cuh kPrec*: 0 = 1xTF32, 1 = 3xTF32, 2 = BF16x9).
 struct TcChoice {
   int cg;
   int bn_cta;
-  bool split3;
+  int prec;
   bool streamk;  // stream-K decomposition (wave-quantized shapes)
 };
 

@@ -92,12 +92,12 @@ tm_status tm_sgemm_tune(int opa, int opb, int64_t m, int64_t n, int64_t k, float
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float best = 1e30f;
-  TcChoice choice{0, 0, true, false};
+  TcChoice choice{0, 0, 1, false};
   tm_status st = TM_OK;
   std::vector<TcChoice> cands;
   for (int cg : {2, 1})
     for (int bn : {128, 64, 32})
-      for (int sk : {0, 1}) cands.push_back(TcChoice{cg, bn, true, sk == 1});
+      for (int sk : {0, 1}) cands.push_back(TcChoice{cg, bn, 1, sk == 1});
   std::vector<std::vector<float>> times(cands.size());
   std::vector<bool> ok(cands.size(), true);
   // rounds interleave the candidates (clock / power drift hits all alike);
@@ -192,7 +192,7 @@ int tm_tune_cache_load(const char* path) {
     if (m <= 0 || n <= 0 || k <= 0 || (ta | tb | bnz) > 1 || ta < 0 || tb < 0 || bnz < 0 || sms <= 0 ||
         !tmk::valid_choice(cg, bn, sk))
       continue;  // malformed entries are skipped
-    tmk::cache()[tmk::Key{m, n, k, ta, tb, bnz, sms}] = TcChoice{cg, bn, true, sk == 1};
+    tmk::cache()[tmk::Key{m, n, k, ta, tb, bnz, sms}] = TcChoice{cg, bn, 1, sk == 1};
     ++loaded;
   }
   std::fclose(f);
