@@ -279,6 +279,21 @@ tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float a
                         const float* A_local, int64_t lda, float* B, int64_t ldb, int root,
                         float beta, float* C_local, int64_t ldc, void* stream);
 
+/* Fused single-launch variant of tm_sgemm_dist (same arguments and result;
+ * SURVEY.md 8(e) "Fused alternative"): ONE persistent tensor-core GEMM over
+ * the full K runs while B's K-chunks are broadcast; after each chunk the comm
+ * stream sets a device flag with a stream memory operation
+ * (cuStreamWriteValue32) and the GEMM's TMA producers wait for chunk c's flag
+ * before loading any stage of it.  No beta chain (C read and written once)
+ * and one launch tail instead of one per chunk.  The GEMM leaves SMs free for
+ * the NCCL kernels.  Falls back to the chunked schedule when the operands do
+ * not meet the tensor-core layout rules.  A transfer that never completes
+ * makes the GEMM trap after ~20 s (TM_ERR_CUDA at the next synchronisation)
+ * instead of hanging the device. */
+tm_status tm_sgemm_dist_fused(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha,
+                              const float* A_local, int64_t lda, float* B, int64_t ldb, int root,
+                              float beta, float* C_local, int64_t ldc, void* stream);
+
 /* Single-process loopback of the distributed mode (verification, DESIGN.md
  * section 10): emulates `nranks` ranks one after another on the CURRENT device
  * with the identical partition, schedule and beta chain as the NCCL entry
@@ -287,6 +302,11 @@ tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float a
  *           chunk by chunk ("broadcast").
  *   mode 1: tm_sgemm_dist_allgather -- Bs[r] holds rank r's k-row shard at rows
  *           [r*k/P, (r+1)*k/P) (k % nranks == 0); every Bs[r] ends complete.
+ *   mode 2: tm_sgemm_dist_fused -- as mode 0, with one flag-gated GEMM per
+ *           rank; the chunk copies (copy-engine transport, no SMs) and the
+ *           flag writes run on a separate stream concurrently with it.
+ *   Env TM_LOOPBACK_LINK_GBS (projections only): each chunk additionally takes
+ *   bytes / rate on the transfer stream, modelling a link of that rate.
  *   A_locals[r], Bs[r], C_locals[r]: device pointers (host arrays of nranks),
  *   shaped as the NCCL entry's A_local, B / B_full, C_local for rank r.
  *   bytes_received: optional host array of nranks counters (bytes each rank's

@@ -28,7 +28,7 @@ lib_path = os.path.join(_PKG, "_lib", "libtm.so")
 EXPORTED_SYMBOLS = [
     "tm_sgemm", "tm_sgemm_ex", "tm_sgemm_op", "tm_sgemm_colmajor", "tm_conv2d_nhwc", "tm_sgemm_host", "tm_release_workspace", "tm_status_string", "tm_get_version",
     "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
-    "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
+    "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_fused", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
     "tm_sgemm_tune", "tm_tune_cache_size", "tm_tune_cache_clear", "tm_tune_cache_save", "tm_tune_cache_load",
     "tm_sgemm_plan_config",
 ]
@@ -67,6 +67,7 @@ def _load():
     L.tm_comm_check.argtypes = [vp, ci]
     L.tm_comm_bytes_received.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
     L.tm_sgemm_dist.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, i64, ci, f32, vp, i64, vp]
+    L.tm_sgemm_dist_fused.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, i64, ci, f32, vp, i64, vp]
     L.tm_sgemm_dist_loopback.argtypes = [ci, ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp, vp]
     L.tm_sgemm_dist_allgather.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, vp, i64, f32, vp, i64, vp]
     pi = ctypes.POINTER(ci)
@@ -354,17 +355,19 @@ def dist_chunks(k: int, nranks: int):
     return out
 
 
-def sgemm_dist_loopback(m, n, k, A_locals, Bs, C_locals, alpha=1.0, beta=0.0, root=0, stream=None, allgather=False):
+def sgemm_dist_loopback(m, n, k, A_locals, Bs, C_locals, alpha=1.0, beta=0.0, root=0, stream=None, allgather=False,
+                        fused=False):
     """Single-process emulation of the row-sharded mode:
     len(A_locals) simulated ranks on the current GPU, same schedule as
     Comm.sgemm (or Comm.sgemm_allgather when allgather=True: Bs[r] holds rank
-    r's k-row shard in place).  Returns the bytes each simulated rank received."""
+    r's k-row shard in place; or Comm.sgemm(fused=True)'s flag-gated single
+    launch when fused=True).  Returns the bytes each simulated rank received."""
     P = len(A_locals)
     arr = lambda ts: (ctypes.c_void_p * P)(*[t.data_ptr() for t in ts])
     lda = next((_ld(a) for a in A_locals if a.shape[0] > 0), max(k, 1))
     ldc = next((_ld(c) for c in C_locals if c.shape[0] > 0), max(n, 1))
     got = (ctypes.c_uint64 * P)()
-    st = lib.tm_sgemm_dist_loopback(P, int(root), 1 if allgather else 0, m, n, k, float(alpha), arr(A_locals), lda,
+    st = lib.tm_sgemm_dist_loopback(P, int(root), 1 if allgather else 2 if fused else 0, m, n, k, float(alpha), arr(A_locals), lda,
                                     arr(Bs), _ld(Bs[0]),
                                     float(beta), arr(C_locals), ldc, got, _stream(stream))
     _check(st, "tm_sgemm_dist_loopback")
@@ -421,16 +424,19 @@ class Comm:
         _check(lib.tm_comm_bytes_received(self.handle, ctypes.byref(v)), "tm_comm_bytes_received")
         return int(v.value)
 
-    def sgemm(self, m, n, k, A_local, B, C_local, alpha=1.0, beta=0.0, root=0, stream=None):
+    def sgemm(self, m, n, k, A_local, B, C_local, alpha=1.0, beta=0.0, root=0, stream=None, fused=False):
         """Row-sharded C_local <- alpha*A_local@B + beta*C_local; B broadcast from root.
 
+        fused=False: K-chunked schedule (one GEMM per chunk, beta chain);
+        fused=True: one flag-gated GEMM over the full K (tm_sgemm_dist_fused).
         Whole rows of B (ldb floats, padding included) are broadcast: B must be a
         k*ldb buffer on every rank (tm.h); use a dense B (ldb == n) for views."""
-        st = lib.tm_sgemm_dist(self.handle, m, n, k, float(alpha), _ptr(A_local),
-                               _ld(A_local) if A_local is not None and A_local.shape[0] > 0 else max(k, 1),
-                               _ptr(B), _ld(B), int(root), float(beta), _ptr(C_local),
-                               _ld(C_local) if C_local.shape[0] > 0 else max(n, 1), _stream(stream))
-        _check(st, "tm_sgemm_dist")
+        fn = lib.tm_sgemm_dist_fused if fused else lib.tm_sgemm_dist
+        st = fn(self.handle, m, n, k, float(alpha), _ptr(A_local),
+                _ld(A_local) if A_local is not None and A_local.shape[0] > 0 else max(k, 1),
+                _ptr(B), _ld(B), int(root), float(beta), _ptr(C_local),
+                _ld(C_local) if C_local.shape[0] > 0 else max(n, 1), _stream(stream))
+        _check(st, "tm_sgemm_dist_fused" if fused else "tm_sgemm_dist")
         return C_local
 
     def sgemm_allgather(self, m, n, k, A_local, B_shard, B_full, C_local, alpha=1.0, beta=0.0, stream=None):

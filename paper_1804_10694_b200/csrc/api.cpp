@@ -251,7 +251,9 @@ bool tc_plan_ok(const GemmArgs& a) { return make_plan(a, TM_ALGO_TF32X3, 148).pa
 
 tm_status sgemm_reserve(const GemmArgs& a, cudaStream_t stream, int sm_reserve) {
   try {
-    return run(a, TM_ALGO_AUTO, stream, sm_reserve);
+    // a gated (fused distributed) GEMM must take the tensor-core kernel, whose
+    // producers honour the chunk flags
+    return run(a, a.kflags ? TM_ALGO_TF32X3 : TM_ALGO_AUTO, stream, sm_reserve);
   } catch (...) {
     return TM_ERR_INTERNAL;
   }

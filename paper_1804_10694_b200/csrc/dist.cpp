@@ -16,6 +16,7 @@
 // all registers) for the whole chunk, so a concurrently enqueued NCCL kernel
 // could not start until it finished -- no overlap.  The communicator is created
 // with maxCTAs = kCommCtas and the chunk GEMMs leave kCommCtas SMs free.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nvtx3/nvToolsExt.h>
@@ -104,6 +105,57 @@ bool nccl() {
 
 constexpr int kMaxChunks = 16;
 
+// cuStreamWriteValue32 through the runtime's driver entry-point query (no
+// link-time libcuda dependency): the transfer stream publishes "chunk c has
+// arrived" with a stream memory operation (no kernel, no SM), ordered after the
+// chunk's transfer on that stream.
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<WriteValue32Fn>(p);
+    return static_cast<WriteValue32Fn>(nullptr);
+  }();
+  return fn;
+}
+tm_status set_flag(cudaStream_t s, unsigned* flag, unsigned value) {
+  WriteValue32Fn fn = write_value32();
+  if (!fn) return TM_ERR_CUDA;
+  return fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0) == CUDA_SUCCESS ? TM_OK
+                                                                                                    : TM_ERR_CUDA;
+}
+
+// Loopback link model (projection only, TM_LOOPBACK_LINK_GBS): after each
+// chunk's on-device copy the transfer stream spins for bytes / rate, so the
+// chunk "arrives" no earlier than a link of that rate would deliver it (the
+// copy's own time comes on top: a conservative model).
+__global__ void k_link_delay(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(500);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+// SMs the loopback's fused GEMM leaves free for its transfers: a same-device
+// cudaMemcpyAsync runs on SMs (measured: with 2 free SMs the 1 GiB broadcast
+// took ~10 ms), so the loopback reserves as many as the NCCL mode does
+// (TM_LOOPBACK_RESERVE overrides; the link-model delay kernel needs one).
+int loopback_reserve() {
+  static const int v = [] {
+    const char* e = std::getenv("TM_LOOPBACK_RESERVE");
+    return e ? std::max(1, std::atoi(e)) : comm_ctas();
+  }();
+  return v;
+}
+double loopback_link_gbs() {
+  const char* e = std::getenv("TM_LOOPBACK_LINK_GBS");
+  return e ? std::atof(e) : 0.0;
+}
+
 }  // namespace
 
 struct tm_comm_s {
@@ -113,6 +165,8 @@ struct tm_comm_s {
   cudaEvent_t ev_start = nullptr;
   cudaEvent_t ev_chunk[kMaxChunks] = {};
   uint64_t bytes_received = 0;
+  unsigned* chunk_flags = nullptr;  // [kMaxChunks] device arrival flags (fused mode)
+  unsigned epoch = 0;               // fused-mode call counter (the flag value of this call)
 };
 
 extern "C" {
@@ -164,6 +218,8 @@ tm_status tm_comm_init(tm_comm_t* out, int nranks, int rank, const tm_unique_id*
             cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) == cudaSuccess;
   for (int i = 0; ok && i < kMaxChunks; ++i)
     ok = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaMalloc(&c->chunk_flags, kMaxChunks * sizeof(unsigned)) == cudaSuccess &&
+       cudaMemset(c->chunk_flags, 0, kMaxChunks * sizeof(unsigned)) == cudaSuccess;
   if (!ok) {
     tm_comm_destroy(c);
     return TM_ERR_CUDA;
@@ -181,6 +237,7 @@ tm_status tm_comm_destroy(tm_comm_t c) {
     if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->chunk_flags) cudaFree(c->chunk_flags);
   delete c;
   return st;
 }
@@ -309,6 +366,65 @@ tm_status dist_schedule(int nranks, int rank, int root, int64_t m, int64_t n, in
   return TM_OK;
 }
 
+// Fused single-launch schedule (SURVEY.md 8(e) "Fused alternative"): ONE
+// persistent GEMM over the full K on `stream`, while B's K-chunks arrive on
+// `comm_stream`; after each chunk's transfer a stream memory operation sets
+// flags[c] = epoch, and the GEMM's TMA producers wait for that flag before they
+// load any stage of chunk c (tc_gemm.cuh wait_chunk_flag).  Unlike the chunked
+// schedule there is one launch tail instead of nchunks and C is read and
+// written once (no beta chain); the cost is that the first wave of tiles is
+// paced by the transfer.  The root's GEMM is not gated (its B is complete).
+// Falls back to the chunked schedule when the tensor-core path cannot take the
+// operands (alignment).  reserve: SMs left to the transfer kernels (NCCL); the
+// copy-engine loopback transport needs none.
+template <class Xfer>
+tm_status dist_fused_schedule(int nranks, int rank, int root, int64_t m, int64_t n, int64_t k, float alpha,
+                              const float* A_local, int64_t lda, float* B, int64_t ldb, float beta, float* C_local,
+                              int64_t ldc, cudaStream_t stream, cudaStream_t comm_stream, cudaEvent_t ev_start,
+                              cudaEvent_t* ev_chunk, unsigned* flags, unsigned epoch, int reserve,
+                              uint64_t* bytes_received, Xfer&& xfer) {
+  int64_t row0 = 0, rows = 0;
+  tm_dist_rows(m, nranks, rank, &row0, &rows);
+  const bool reads_ab = alpha != 0.0f && k > 0 && n > 0;
+  if (!reads_ab || nranks == 1)
+    return tm_sgemm(rows, n, k, alpha, A_local, lda, B, ldb, beta, C_local, ldc, stream);
+  if (!B || ldb < (n > 1 ? n : 1)) return TM_ERR_INVALID_VALUE;
+  tmk::GemmArgs ga{rows, n, k, alpha, beta, A_local, lda, B, ldb, C_local, ldc};
+  if (rows > 0 && !tmk::tc_plan_ok(ga))
+    return dist_schedule(nranks, rank, root, m, n, k, alpha, A_local, lda, B, ldb, beta, C_local, ldc, stream,
+                         comm_stream, ev_start, ev_chunk, bytes_received, xfer);
+  int64_t nchunks = 0, kc = 0;
+  tm_dist_chunk(k, nranks, -1, &nchunks, &kc);
+  if (nchunks > kMaxChunks) return TM_ERR_INTERNAL;
+  if (cudaEventRecord(ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (cudaStreamWaitEvent(comm_stream, ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
+  nvtxRangePushA("tm_sgemm_dist fused schedule");
+  struct Pop {
+    ~Pop() { nvtxRangePop(); }
+  } pop;
+  int c = 0;
+  for (int64_t k0 = 0; k0 < k; k0 += kc, ++c) {
+    const int64_t kr = (k0 + kc <= k) ? kc : k - k0;
+    const size_t count = static_cast<size_t>(kr) * static_cast<size_t>(ldb);
+    tm_status st = xfer(B + k0 * ldb, count);
+    if (st != TM_OK) return st;
+    if (rank != root && bytes_received) *bytes_received += count * 4;
+    if ((st = set_flag(comm_stream, flags + c, epoch)) != TM_OK) return st;
+  }
+  if (cudaEventRecord(ev_chunk[0], comm_stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (rows > 0) {
+    if (rank != root) {
+      ga.kflags = flags;
+      ga.kepoch = epoch;
+      ga.kchunk = kc;
+    }
+    tm_status st = tmk::sgemm_reserve(ga, stream, reserve);
+    if (st != TM_OK) return st;
+  }
+  // the call completes (stream-ordered) only when B has fully arrived
+  return cudaStreamWaitEvent(stream, ev_chunk[0], 0) == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+}
+
 // All-gather variant: B arrives pre-sharded by k-rows (rank r owns rows
 // [r*kr, (r+1)*kr), kr = k/P).  The GEMM on the own shard needs no
 // communication and runs first, overlapping the gather (`gather()` enqueues it
@@ -368,12 +484,25 @@ tm_status tm_sgemm_dist(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float a
                        &comm->bytes_received, xfer);
 }
 
+tm_status tm_sgemm_dist_fused(tm_comm_t comm, int64_t m, int64_t n, int64_t k, float alpha, const float* A_local,
+                              int64_t lda, float* B, int64_t ldb, int root, float beta, float* C_local, int64_t ldc,
+                              void* stream_) {
+  if (!comm || root < 0 || root >= comm->nranks || m < 0 || n < 0 || k < 0) return TM_ERR_INVALID_VALUE;
+  auto xfer = [&](float* p, size_t count) -> tm_status {
+    return g_nccl.Broadcast(p, p, count, ncclFloat32, root, comm->comm, comm->stream) == ncclSuccess ? TM_OK
+                                                                                                    : TM_ERR_NCCL;
+  };
+  return dist_fused_schedule(comm->nranks, comm->rank, root, m, n, k, alpha, A_local, lda, B, ldb, beta, C_local,
+                             ldc, static_cast<cudaStream_t>(stream_), comm->stream, comm->ev_start, comm->ev_chunk,
+                             comm->chunk_flags, ++comm->epoch, comm_ctas(), &comm->bytes_received, xfer);
+}
+
 tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int64_t n, int64_t k, float alpha,
                                  const float* const* A_locals, int64_t lda, float* const* Bs, int64_t ldb,
                                  float beta, float* const* C_locals, int64_t ldc, uint64_t* bytes_received,
                                  void* stream_) {
   if (nranks < 1 || root < 0 || root >= nranks || !A_locals || !Bs || !C_locals || m < 0 || n < 0 || k < 0 ||
-      (mode != 0 && mode != 1))
+      mode < 0 || mode > 2)
     return TM_ERR_INVALID_VALUE;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   cudaStream_t cs = nullptr;
@@ -383,7 +512,12 @@ tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int6
             cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) == cudaSuccess;
   for (int i = 0; ok && i < kMaxChunks; ++i)
     ok = cudaEventCreateWithFlags(&ev_chunk[i], cudaEventDisableTiming) == cudaSuccess;
+  unsigned* flags = nullptr;  // fused mode: per-chunk arrival flags, zeroed once (rank r's epoch is r + 1)
+  if (ok && mode == 2)
+    ok = cudaMalloc(&flags, kMaxChunks * sizeof(unsigned)) == cudaSuccess &&
+         cudaMemsetAsync(flags, 0, kMaxChunks * sizeof(unsigned), stream) == cudaSuccess;
   if (!ok) st = TM_ERR_CUDA;
+  const double link_gbs = loopback_link_gbs();
   if (bytes_received)
     for (int r = 0; r < nranks; ++r) bytes_received[r] = 0;
   // Ranks run one after another on this device; rank r's "broadcast" copies
@@ -402,15 +536,25 @@ tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int6
     if (st == TM_OK && cudaStreamSynchronize(stream) != cudaSuccess) st = TM_ERR_CUDA;
   }
   for (int r = 0; st == TM_OK && r < nranks; ++r) {
-    if (mode == 0) {
+    if (mode == 0 || mode == 2) {
       const float* root_B = Bs[root];
       auto xfer = [&](float* p, size_t count) -> tm_status {
         if (r == root) return TM_OK;
         const float* src = root_B + (p - Bs[r]);
-        return cudaMemcpyAsync(p, src, count * 4, cudaMemcpyDeviceToDevice, cs) == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+        if (cudaMemcpyAsync(p, src, count * 4, cudaMemcpyDeviceToDevice, cs) != cudaSuccess) return TM_ERR_CUDA;
+        if (link_gbs > 0.0) {  // projection: the chunk arrives at the modelled link rate
+          k_link_delay<<<1, 1, 0, cs>>>(static_cast<unsigned long long>(count * 4.0 / link_gbs));
+          if (cudaGetLastError() != cudaSuccess) return TM_ERR_CUDA;
+        }
+        return TM_OK;
       };
-      st = dist_schedule(nranks, r, root, m, n, k, alpha, A_locals[r], lda, Bs[r], ldb, beta, C_locals[r], ldc,
-                         stream, cs, ev_start, ev_chunk, bytes_received ? &bytes_received[r] : nullptr, xfer);
+      if (mode == 0)
+        st = dist_schedule(nranks, r, root, m, n, k, alpha, A_locals[r], lda, Bs[r], ldb, beta, C_locals[r], ldc,
+                           stream, cs, ev_start, ev_chunk, bytes_received ? &bytes_received[r] : nullptr, xfer);
+      else  // flags of simulated rank r carry epoch r + 1 (flags are never reset within the call)
+        st = dist_fused_schedule(nranks, r, root, m, n, k, alpha, A_locals[r], lda, Bs[r], ldb, beta, C_locals[r],
+                                 ldc, stream, cs, ev_start, ev_chunk, flags, static_cast<unsigned>(r + 1),
+                                 loopback_reserve(), bytes_received ? &bytes_received[r] : nullptr, xfer);
     } else {
       auto gather = [&](size_t count) -> tm_status {
         for (int q = 0; q < nranks; ++q) {
@@ -429,6 +573,7 @@ tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int6
   }
   if (shards) cudaFree(shards);
   if (cs) cudaStreamSynchronize(cs);
+  if (flags) cudaFree(flags);
   for (int i = 0; i < kMaxChunks; ++i)
     if (ev_chunk[i]) cudaEventDestroy(ev_chunk[i]);
   if (ev_start) cudaEventDestroy(ev_start);

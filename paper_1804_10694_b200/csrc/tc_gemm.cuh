@@ -130,6 +130,11 @@ struct TcParams {
   unsigned long long* trace;  // debug timeline [grid][kTraceSlots] (%globaltimer ns) or null
   unsigned* wave_ctr;         // data-parallel wave barrier counter (zeroed per launch) or null
   int full_waves;             // waves in which every cluster has a tile
+  // fused distributed mode: B's K-chunk c (kchunk_blocks K-blocks) may be read
+  // once kflags[c] >= kepoch (set by the transfer stream); null otherwise
+  const unsigned* kflags;
+  unsigned kepoch;
+  int kchunk_blocks;
   // implicit-GEMM convolution (CONV kernels): GEMM row = output pixel
   // (b, y, x) of an Nb x Ho x Wo grid, K index = (ky*S + kx)*C + c.
   int cv_ho, cv_wo, cv_s, cv_c, cv_pad;
@@ -300,6 +305,23 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 }
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Fused distributed mode: wait until B's K-chunk c has arrived (its flag,
+// written by a stream memory operation after the chunk's transfer, reaches
+// this call's epoch), then order the TMA (async-proxy) reads of that chunk
+// after the acquire.  A transfer that never completes traps after ~20 s
+// instead of hanging the device.
+static __device__ __noinline__ void wait_chunk_flag(const unsigned* flag, unsigned epoch) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (static_cast<int>(ld_acquire_gpu(flag) - epoch) < 0) {
+    __nanosleep(200);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) __trap();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ epilogue
@@ -556,6 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         UnitIter ui = units_begin(p, cluster_id, num_clusters);
         Unit u;
         int wi = 0;
+        int chunk_ready = -1;  // fused distributed mode: highest B chunk known to be present
         while (units_next(p, num_clusters, ui, u)) {
           if (pi == 0 && p.wave_ctr && wi >= 1 && wi < p.full_waves) {
             // Keep the persistent clusters in step at tile boundaries so the
@@ -572,6 +595,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int rows_here = min(kBMCta, p.m - row0);
           for (int kb = u.kb0; kb < u.kb1; ++kb) {
             if (own == pi) {
+              if (p.kflags) {
+                const int c = kb / p.kchunk_blocks;
+                if (c > chunk_ready) {
+                  wait_chunk_flag(p.kflags + c, p.kepoch);
+                  chunk_ready = c;
+                }
+              }
               if (kb == max(u.kb0, u.kb1 - p.kc_blocks) && u.kb0 == 0 && p.beta != 0.0f && rows_here > 0) {
                 // This unit ends in the epilogue (a whole tile or a stream-K
                 // finalizer) and will read beta*C: stage this CTA's C rows
@@ -1065,6 +1095,10 @@ tm_status launch_cfg(const GemmArgs& a, int num_sms, bool streamk, cudaStream_t 
   p.beta = a.beta;
   p.C = a.C;
   p.ldc = a.ldc;
+  p.kflags = a.kflags;
+  p.kepoch = a.kepoch;
+  p.kchunk_blocks = static_cast<int>(a.kchunk / kBK);
+  if (a.kflags && (a.kchunk <= 0 || a.kchunk % kBK != 0)) return TM_ERR_INVALID_VALUE;
   return launch_kernel<CG, BN_CTA, PREC, TA, TB, 32, false>(tmA, tmB, p, num_sms, streamk, stream);
 }
 

@@ -37,6 +37,12 @@ struct GemmArgs {
   float* C;
   int64_t ldc;
   bool ta = false, tb = false;
+  // Fused distributed mode (dist.cpp): B arrives in K-chunks of kchunk rows
+  // while the GEMM runs; chunk c is present once kflags[c] >= kepoch (written
+  // by the transfer stream).  Tensor-core path only (kflags == nullptr: none).
+  const unsigned* kflags = nullptr;
+  unsigned kepoch = 0;
+  int64_t kchunk = 0;
 };
 
 // Tensor-core configuration: CTA group (1 or 2), B columns per CTA (32/64/128),
@@ -66,7 +72,8 @@ tm_status launch_scale(int64_t m, int64_t n, float beta, float* C, int64_t ldc, 
 tm_status launch_l2_flush(const float* buf, int64_t bytes, cudaStream_t stream);
 
 // tm_sgemm with `sm_reserve` SMs left free (distributed mode, so the NCCL
-// broadcast kernels can run concurrently with the persistent GEMM).
+// broadcast kernels can run concurrently with the persistent GEMM).  With
+// a.kflags set (fused distributed mode) it runs the tensor-core path only.
 tm_status sgemm_reserve(const GemmArgs& a, cudaStream_t stream, int sm_reserve);
 
 // Library-owned stream-K workspace for `stream` on the current device: at least

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-def _run(P, root, m, n, k, seed, kind="uniform", ldb=None):
+def _run(P, root, m, n, k, seed, kind="uniform", ldb=None, fused=False):
     import torch
     import paper_1804_10694_b200 as tm
     ldb = n if ldb is None else ldb
@@ -34,15 +34,18 @@ def _run(P, root, m, n, k, seed, kind="uniform", ldb=None):
             Bs.append(torch.from_numpy(Bfull).cuda())
         else:
             Bs.append(torch.full((k, ldb), float("nan"), dtype=torch.float32, device="cuda"))
-    got = tm.sgemm_dist_loopback(m, n, k, As, [b for b in Bs], Cs, si.ALPHA, si.BETA, root=root)
+    got = tm.sgemm_dist_loopback(m, n, k, As, [b for b in Bs], Cs, si.ALPHA, si.BETA, root=root, fused=fused)
     torch.cuda.synchronize()
     return A, B, C0, parts, [c.cpu().numpy() for c in Cs], got, [b[:, :n].cpu().numpy() for b in Bs]
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("P,root", [(2, 0), (3, 1), (8, 0), (8, 5)])
-def test_loopback_shards_match_oracle(P, root):
+def test_loopback_shards_match_oracle(P, root, fused):
+    """fused=False: K-chunked schedule (beta chain); fused=True: one GEMM per
+    rank whose TMA producers wait on per-chunk flags set by the copy stream."""
     m, n, k = 1060, 260, 1100   # uneven rows; two K-chunks of 576 and 524
-    A, B, C0, parts, Cs, got, Bs = _run(P, root, m, n, k, seed=40 + P)
+    A, B, C0, parts, Cs, got, Bs = _run(P, root, m, n, k, seed=40 + P, fused=fused)
     R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0)
     for r, ((r0, rows), C) in enumerate(zip(parts, Cs)):
         assert C.shape == (rows, n)
@@ -73,7 +76,8 @@ def test_loopback_more_ranks_than_rows():
             assert float(np.max(oracle.normalized_error(C, R[r0:r0 + rows], D[r0:r0 + rows]))) <= TOL
 
 
-def test_loopback_c5_p8_sampled_rows():
+@pytest.mark.parametrize("fused", [False, True])
+def test_loopback_c5_p8_sampled_rows(fused):
     """BASELINE.json configs[4]: 16384^3 row-sharded over 8 ranks (8 chunks of
     2048), sampled rows incl. every shard boundary, all-positive stress data
     (the beta chain adds 7 extra fp32 roundings per element)."""
@@ -91,7 +95,7 @@ def test_loopback_c5_p8_sampled_rows():
         bounds += [r0, r0 + rows - 1]
         As.append(dA[r0:r0 + rows])
         Cs.append(torch.from_numpy(C0[r0:r0 + rows].copy()).cuda())
-    tm.sgemm_dist_loopback(m, n, k, As, Bs, Cs, si.ALPHA, si.BETA)
+    tm.sgemm_dist_loopback(m, n, k, As, Bs, Cs, si.ALPHA, si.BETA, fused=fused)
     C = torch.cat(Cs).cpu().numpy()
     del Bs, dA, dB, As, Cs
     torch.cuda.empty_cache()
@@ -127,3 +131,21 @@ def test_loopback_allgather_shards_match_oracle(P):
         assert e <= TOL, (r, e)
         assert np.array_equal(Bs[r].cpu().numpy(), B)
         assert got[r] == (P - 1) * kr * n * 4
+
+
+def test_loopback_fused_many_chunks_and_slow_link():
+    """Fused mode with 8 chunks, misaligned-free but ragged tiles, and the
+    transfer slowed to a modelled 200 GB/s link (TM_LOOPBACK_LINK_GBS): the
+    gated GEMM must wait for every chunk and still match the oracle; integer
+    inputs bit-exact (one GEMM per rank: no beta chain roundings)."""
+    import os
+    os.environ["TM_LOOPBACK_LINK_GBS"] = "200"
+    try:
+        m, n, k = 777, 300, 4100  # 8 chunks of 544 rows, ragged last
+        A, B, C0, parts, Cs, got, Bs = _run(4, 2, m, n, k, seed=70, kind="integer", fused=True)
+    finally:
+        del os.environ["TM_LOOPBACK_LINK_GBS"]
+    R, _ = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0)
+    for r, ((r0, rows), C) in enumerate(zip(parts, Cs)):
+        assert np.array_equal(C.astype(np.float64), R[r0:r0 + rows]), r
+        assert got[r] == (0 if r == 2 else k * n * 4)

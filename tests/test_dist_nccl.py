@@ -43,11 +43,13 @@ def test_one_rank_comm_lifecycle_and_sgemm():
         dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
         dC = torch.from_numpy(C0).cuda()
         comm.sgemm(m, n, k, dA, dB, dC, si.ALPHA, si.BETA, root=0)
+        dCf = torch.from_numpy(C0).cuda()
+        comm.sgemm(m, n, k, dA, dB, dCf, si.ALPHA, si.BETA, root=0, fused=True)
         ref = torch.from_numpy(C0).cuda()
         tm.sgemm(dA, dB, ref, si.ALPHA, si.BETA)
         torch.cuda.synchronize()
         assert _err(dC.cpu().numpy(), R, D) <= TOL
-        assert torch.equal(dC, ref)  # P = 1 is exactly tm_sgemm
+        assert torch.equal(dC, ref) and torch.equal(dCf, ref)  # P = 1 is exactly tm_sgemm
         # all-gather variant at P = 1: the one shard is all of B (ncclAllGather
         # copies it into B_full), then the GEMM
         B_full = torch.full((k, n), float("nan"), device="cuda")
@@ -97,6 +99,13 @@ def _worker(rank, world, port, q):
         out["bcast_B_equal"] = bool(np.array_equal(dB.cpu().numpy(), B))
         out["bcast_bytes"] = comm.bytes_received()
         out["bcast_bytes_expected"] = 0 if rank == root else k * n * 4
+        # fused single launch (flag-gated GEMM), root 0, same data
+        dCf = torch.from_numpy(np.ascontiguousarray(C0[r0:r0 + rows])).cuda()
+        dBf = torch.from_numpy(B).cuda() if rank == 0 else torch.full((k, n), float("nan"), device="cuda")
+        comm.sgemm(m, n, k, dA, dBf, dCf, si.ALPHA, si.BETA, root=0, fused=True)
+        torch.cuda.synchronize()
+        out["fused_err"] = _err(dCf.cpu().numpy(), R, D)
+        out["fused_B_equal"] = bool(np.array_equal(dBf.cpu().numpy(), B))
         # all-gather variant: rank r holds k-rows [r*k/P, (r+1)*k/P) of B
         k2 = 256 * world
         A2, B2, C2 = si.matrices(m, n, k2, seed=63)
@@ -141,7 +150,8 @@ def test_multi_rank_nccl_broadcast_and_allgather():
         o = res[r]
         assert "error" not in o, o
         assert o["bcast_err"] <= TOL and o["ag_err"] <= TOL, o
-        assert o["bcast_B_equal"] and o["ag_B_equal"], o
+        assert o["bcast_B_equal"] and o["ag_B_equal"] and o["fused_B_equal"], o
+        assert o["fused_err"] <= TOL, o
         assert o["bcast_bytes"] == o["bcast_bytes_expected"], o
         assert o["ag_bytes"] == o["ag_bytes_expected"], o
         assert o["check"], o
