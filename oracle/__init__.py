@@ -82,6 +82,8 @@ def _load():
         lib.tm_oracle_dist_rows.argtypes = [i64, ctypes.c_int, ctypes.c_int,
                                             ctypes.POINTER(i64), ctypes.POINTER(i64)]
         lib.tm_oracle_dist_rows.restype = ctypes.c_int
+        lib.tm_oracle_blur.argtypes = [i64, i64, vp, i64, vp, vp, vp]
+        lib.tm_oracle_blur.restype = ctypes.c_int
         lib.tm_oracle_set_threads.argtypes = [ctypes.c_int]
         lib.tm_oracle_get_threads.restype = ctypes.c_int
         _lib = lib
@@ -169,6 +171,24 @@ def conv2d_nhwc(alpha, X, Wt, beta, Y0, pad, pixels=None):
     if rc != 0:
         raise ValueError(f"tm_oracle_conv2d_nhwc rejected its arguments (rc={rc})")
     return Rr, Dd
+
+
+def blur(img, rows=None):
+    """R, D (fp64, shape (len(rows) or N-2, M-2, 3)) of the paper's two-stage
+    blur of an N x M x 3 float32 image (oracle.c tm_oracle_blur)."""
+    img = np.ascontiguousarray(img, dtype=np.float32)
+    N, M, C = img.shape
+    assert C == 3
+    if rows is None:
+        nrows, r = N - 2, None
+    else:
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        nrows = r.shape[0]
+    R = np.empty((nrows, M - 2, 3), np.float64)
+    D = np.empty((nrows, M - 2, 3), np.float64)
+    if _load().tm_oracle_blur(N, M, _ptr(img), nrows, _ptr(r), _ptr(R), _ptr(D)) != 0:
+        raise ValueError("tm_oracle_blur rejected its arguments")
+    return R, D
 
 
 def dist_rows(m, nranks, rank):

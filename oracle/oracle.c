@@ -66,7 +66,8 @@
  *    3 op(B) read transposed             9 conv: padding not subtracted from the input row
  *    4 lda ignored (A read as dense)    10 dist_rows: the m mod P extra rows go to the LAST ranks
  *    5 fabs dropped from D              11 beta == 0 still reads C0
- *    6 beta term subtracted */
+ *    6 beta term subtracted             12 blur: bx reads in(i, j+1) instead of in(i, j+2)
+ *                                       13 blur: by's average misses its /3 */
 #ifndef ORACLE_MUTANT
 #define ORACLE_MUTANT 0
 #endif
@@ -280,6 +281,49 @@ int tm_oracle_conv2d_nhwc(int64_t Nb, int64_t H, int64_t W, int64_t C, int64_t F
             }
             Rout[t * F + f] = r;
             Dout[t * F + f] = d;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------
+ * Blur oracle (the paper's distributed example, a
+ * second distributed workload).  PAPER.md:216-219 (Fig. 3, the Blur algorithm):
+ *
+ *   bx(i,j,c) = (in(i,j,c) + in(i,j+1,c) + in(i,j+2,c)) / 3
+ *   by(i,j,c) = (bx(i,j,c) + bx(i+1,j,c) + bx(i+2,j,c)) / 3
+ *   0 <= i < N-2, 0 <= j < M-2, 0 <= c < 3
+ *
+ * written out in fp64 (the paper's element type is not stated; inputs are
+ * fp32).  `in` is N x M x 3 row-major (channels interleaved, in(i,j,c) at
+ * in[(i*M + j)*3 + c]); R (and the tolerance scale D = (1/9) sum of the nine
+ * |in| taps) are (N-2) x (M-2) x 3.  Rows `rows[0..nrows)` of the output only
+ * (NULL: all N-2).  Returns -1 on invalid arguments (N < 3 or M < 3). */
+int tm_oracle_blur(int64_t N, int64_t M, const float *in, int64_t nrows, const int64_t *rows,
+                   double *R, double *D) {
+    if (N < 3 || M < 3 || !in || nrows < 0 || (nrows > 0 && (!R || !D))) return -1;
+    if (!rows && nrows != N - 2) return -1;
+    if (rows)
+        for (int64_t t = 0; t < nrows; ++t)
+            if (rows[t] < 0 || rows[t] >= N - 2) return -1;
+    const int64_t W = M - 2;
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < nrows; ++t) {
+        const int64_t i = rows ? rows[t] : t;
+        for (int64_t j = 0; j < W; ++j) {
+            for (int64_t c = 0; c < 3; ++c) {
+                double bx[3], ax[3];
+                for (int64_t di = 0; di < 3; ++di) {           /* bx(i+di, j, c) */
+                    const float *row = in + ((i + di) * M) * 3;
+                    const double a = row[j * 3 + c], b = row[(j + 1) * 3 + c];
+                    const double e = row[(j + (MUT(12) ? 1 : 2)) * 3 + c];
+                    bx[di] = (a + b + e) / 3.0;
+                    ax[di] = (fabs(a) + fabs(b) + fabs(e)) / 3.0;
+                }
+                const double s = bx[0] + bx[1] + bx[2];
+                R[(t * W + j) * 3 + c] = MUT(13) ? s : s / 3.0;
+                D[(t * W + j) * 3 + c] = (ax[0] + ax[1] + ax[2]) / 3.0;
+            }
         }
     }
     return 0;

@@ -4,7 +4,7 @@ Each mutant is oracle.c compiled with -DORACLE_MUTANT=n (one step broken on
 purpose: a dropped term, a wrong sign or index, a transposed operand, flipped
 filter taps, a padding slip, the partition remainder on the wrong ranks, C0 read
 when beta == 0; the list is in oracle.c's header).  The pin suites
-(tests/test_oracle.py, tests/test_conv_oracle.py) are run against each mutant in
+(tests/test_oracle.py, tests/test_conv_oracle.py, tests/test_blur_oracle.py) are run against each mutant in
 a subprocess through TM_ORACLE_LIB and must FAIL; the same harness on the
 unmutated source (n = 0) must PASS, so a failure is the mutant's doing.
 """
@@ -18,12 +18,13 @@ import pytest
 import oracle
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PINS = ["tests/test_oracle.py", "tests/test_conv_oracle.py"]
+PINS = ["tests/test_oracle.py", "tests/test_conv_oracle.py", "tests/test_blur_oracle.py"]
 MUTANTS = {
     1: "beta term dropped", 2: "last product dropped (k-1)", 3: "op(B) transposed",
     4: "lda ignored for A", 5: "fabs dropped from D", 6: "beta term subtracted",
     7: "alpha dropped", 8: "conv filter taps flipped", 9: "conv padding not subtracted",
     10: "partition remainder to the last ranks", 11: "beta == 0 reads C0",
+    12: "blur bx reads j+1 for j+2", 13: "blur by misses its /3",
 }
 
 
