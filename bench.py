@@ -272,7 +272,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C3b", "C4", "C5", "CONV"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C3b", "C4", "C5", "CONV", "BLUR"])
     ap.add_argument("--algo", default="auto", choices=list(ALGOS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -284,6 +284,8 @@ def main():
         return run_reference(args)
     if args.config == "CONV":
         return run_conv(args)
+    if args.config == "BLUR":
+        return run_blur(args)
 
     import torch
     import torch.distributed as dist
@@ -502,6 +504,118 @@ def run_conv(args):
             "gpu_launches": args.steps,
             "clocks": clocks.summary()}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_blur(args):
+    """The paper's Blur on its 2112x3520 RGB image
+     through tm_blur (N = 1) or the row-distributed tm_blur_dist
+    (N > 1: the Fig. 5 schedule, border rows over NCCL; strong scaling, the image
+    is fixed).  SURVEY.md 8(f) item 3's second distributed workload, not a
+    BASELINE.json config.  Roofline: HBM; algorithmic bytes = the image read once
+    + the output written once, 12 (N M + (N-2)(M-2)) bytes.  The 89 MB image fits
+    in L2, so L2 is flushed (512 MiB read) between steps."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1804_10694_b200 as tm
+    import seeded_inputs as si
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N, M = si.BLUR_IMAGE
+    img = si.image(N, M)
+    r0, rows = tm.dist_rows(N - 2, world, rank)
+    lin = torch.from_numpy(np.ascontiguousarray(img[r0:r0 + rows + 2])).cuda()  # chunk + border region
+    if world > 1 and rank < world - 1:
+        lin[rows:] = float("nan")  # received from rank + 1 every step
+    lout = torch.empty((rows, M - 2, 3), dtype=torch.float32, device="cuda")
+    comm = tm.Comm(rank, world) if world > 1 else None
+    flush = torch.ones(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    flush_out = torch.empty(1, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if comm is None:
+            tm.blur(lin, lout)
+        else:
+            comm.blur(N, M, lin, lout)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        t_soak = time.time()
+        for _ in range(args.warmup):
+            torch.sum(flush, dim=0, out=flush_out[0])
+            step()
+        torch.cuda.synchronize()
+        while time.time() - t_soak < 1.0:
+            for _ in range(8):
+                torch.sum(flush, dim=0, out=flush_out[0])
+                step()
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0_host = time.time()
+        for i in range(args.steps):
+            torch.sum(flush, dim=0, out=flush_out[0])
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks.mark_region(t0_host, time.time())
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([sum(per_step), statistics.median(per_step)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, med_ms = float(t[0].item()), float(t[1].item())
+    algo_bytes = 12 * (N * M + (N - 2) * (M - 2))
+    value = algo_bytes * args.steps / (total_ms * 1e-3) / 1e9
+    my_bytes = 12 * ((rows + 2) * M + rows * (M - 2))
+    my_gbs = my_bytes / (statistics.median(per_step) * 1e-3) / 1e9
+    peaks = load_peaks()
+    traffic, traffic_src = ncu_traffic("BLUR", "blur", world)
+    line = {"metric": "blur GB/s (PAPER.md:216-219 Blur on the 2112x3520 RGB image of PAPER.md:842)",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(total_ms / args.steps, 5),
+            "step_ms": {"median": round(med_ms, 5), "min": round(min(per_step), 5), "max": round(max(per_step), 5)},
+            "mpixels_per_s": round((N - 2) * (M - 2) * args.steps / (total_ms * 1e-3) / 1e6, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded U[0,1) RGB image, numpy PCG64)",
+            "config": {"workload": f"blur {N}x{M}x3 (PAPER.md:842)", "rows_per_rank": rows,
+                       "parallelism": f"row-shard x{world} (Fig. 5 border exchange)" if world > 1 else "single GPU",
+                       "l2": "L2 flushed (512 MiB read) between steps"},
+            "roofline": {"bound": "hbm", "achieved": round(my_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(my_gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
+                         "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
+                         "algorithmic_bytes": my_bytes, "kernel": "k_blur"},
+            "gpu_launches": args.steps * (1 if world == 1 else 2), "clocks": clocks.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        # parity of this run's output on sampled rows, and the oracle's rate on them
+        rows_s = np.unique(np.concatenate([[0, 1, N - 4, N - 3], np.arange(31, N - 2, 32),
+                                           np.random.default_rng(7).integers(0, N - 2, 64)])).astype(np.int64)
+        t0 = time.perf_counter()
+        R, D = oracle.blur(img, rows=rows_s)
+        dt = time.perf_counter() - t0
+        got = lout.cpu().numpy()[rows_s].astype(np.float64)
+        err = float(np.max(np.abs(got - R) / np.where(D == 0, 1.0, D)))
+        line["cpu_baseline"] = {"value": round(12 * len(rows_s) * (2 * M - 2) / dt / 1e9, 3), "unit": "GB/s",
+                                "cores": oracle.get_threads(), "kind": "oracle",
+                                "sample": f"{len(rows_s)} output rows x {M - 2} x 3 ({dt:.2f} s)",
+                                "parity_sample": {"rows": int(len(rows_s)), "max_normalized_error": err,
+                                                  "tolerance": 1e-6, "pass": err <= 1e-6}}
+    if comm is not None:
+        comm.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 

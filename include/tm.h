@@ -329,6 +329,53 @@ tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t 
                                   float* B_full, int64_t ldb, float beta, float* C_local,
                                   int64_t ldc, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Blur: the paper's second distributed workload.
+ *
+ * The two-stage 3x3 box blur of PAPER.md:216-219 (Fig. 3):
+ *     bx(i,j,c) = (in(i,j,c) + in(i,j+1,c) + in(i,j+2,c)) / 3
+ *     by(i,j,c) = (bx(i,j,c) + bx(i+1,j,c) + bx(i+2,j,c)) / 3
+ *     for 0 <= i < N-2, 0 <= j < M-2, 0 <= c < 3
+ * (the paper ignores boundary conditions, so the output is (N-2) x (M-2) x 3).
+ * Layout (the paper's in[i][j][c], channels interleaved): row i of the image
+ * is 3M floats at in + i*ldi, in(i,j,c) = in[i*ldi + 3j + c], ldi >= 3M; row i
+ * of the output is 3(M-2) floats at out + i*ldo, ldo >= 3(M-2).  Device
+ * pointers; `in` spans (N-1)*ldi + 3M floats, `out` (N-3)*ldo + 3(M-2).
+ * Arithmetic: fp32, "/ 3" as a multiply by fl(1/3); |by - exact| <= 1e-6 * D
+ * with D = (1/9) sum of the nine |in| taps (blur accuracy).
+ * Deterministic.  Vector loads/stores are used when in/out are 16-byte aligned
+ * and ldi/ldo multiples of 4 (8-byte / even for 2-wide stores); any alignment
+ * is accepted.
+ * Errors: N < 3, M < 3, NULL pointers, ldi < 3M, ldo < 3(M-2) or out
+ * overlapping in -> TM_ERR_INVALID_VALUE (out untouched). */
+tm_status tm_blur(int64_t N, int64_t M, const float* in, int64_t ldi, float* out, int64_t ldo, void* stream);
+
+/* Row-distributed blur (Fig. 5 Code 3; collective over the
+ * communicator).  The N-2 output rows are partitioned with tm_dist_rows(N-2,
+ * P, r): rank r computes output rows [row0, row0 + rows).  Its local image
+ * `lin` holds rows + 2 rows of pitch ldi: rows [0, rows) are input rows
+ * [row0, row0 + rows) (the rank's chunk); rows [rows,
+ * rows + 2) are the border region: on the last rank the caller fills them
+ * with input rows N-2 and N-1, on every other rank they are OVERWRITTEN with
+ * the first two rows of rank r+1's chunk, received over NCCL (the paper's
+ * send from node is to is-1 / receive at lin(N,0,0) from ir+1, PAPER.md:
+ * 581-582: 2 rows, here ldi + 3M floats).  `lout`: rows x 3(M-2) (pitch ldo).
+ * The interior output rows [0, rows - 2) are computed while the border rows
+ * are in flight; the last two once they have arrived.  No gather of the
+ * output.  Requires (N-2)/P >= 2 when P > 1 (every chunk
+ * holds the two rows its upper neighbour needs), else TM_ERR_INVALID_VALUE.
+ * Stream-ordered; errors as tm_blur, TM_ERR_NCCL on communication failure. */
+tm_status tm_blur_dist(tm_comm_t comm, int64_t N, int64_t M, float* lin, int64_t ldi, float* lout, int64_t ldo,
+                       void* stream);
+
+/* Single-process loopback of tm_blur_dist (verification): `nranks` simulated
+ * ranks on the current device, lins[r] / louts[r] as rank r's lin / lout;
+ * the border-row exchange is a device-to-device copy on a separate stream,
+ * with the identical schedule.  bytes_received: optional host array of nranks
+ * counters.  Synchronises `stream`. */
+tm_status tm_blur_dist_loopback(int nranks, int64_t N, int64_t M, float* const* lins, int64_t ldi,
+                                float* const* louts, int64_t ldo, uint64_t* bytes_received, void* stream);
+
 /* Failure detection: polls the communicator for asynchronous NCCL errors
  * (e.g. a peer died or a network/NVLink fault).  TM_OK if healthy (or an
  * operation is still in progress), TM_ERR_NCCL if an error was reported; with

@@ -16,7 +16,7 @@ import os
 __all__ = [
     "ALGO_AUTO", "ALGO_TF32X3", "ALGO_SIMT_F32", "ALGO_TF32X1", "ALGO_BF16X9", "TmError", "lib", "lib_path", "sgemm",
     "sgemm_ex", "sgemm_host", "plan_name", "plan_config", "tune", "tune_cache_save", "tune_cache_load",
-    "tune_cache_clear", "tune_cache_size", "dist_rows", "Comm", "status_string", "EXPORTED_SYMBOLS",
+    "tune_cache_clear", "tune_cache_size", "dist_rows", "Comm", "blur", "blur_dist_loopback", "status_string", "EXPORTED_SYMBOLS",
 ]
 
 ALGO_AUTO, ALGO_TF32X3, ALGO_SIMT_F32, ALGO_TF32X1, ALGO_BF16X9 = 0, 1, 2, 3, 4
@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = [
     "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
     "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_fused", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
     "tm_sgemm_tune", "tm_tune_cache_size", "tm_tune_cache_clear", "tm_tune_cache_save", "tm_tune_cache_load",
-    "tm_sgemm_plan_config",
+    "tm_sgemm_plan_config", "tm_blur", "tm_blur_dist", "tm_blur_dist_loopback",
 ]
 
 
@@ -77,6 +77,9 @@ def _load():
     L.tm_tune_cache_save.argtypes = [ctypes.c_char_p]
     L.tm_tune_cache_load.argtypes = [ctypes.c_char_p]
     L.tm_sgemm_plan_config.argtypes = [ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, ci, pi, pi, pi, pi]
+    L.tm_blur.argtypes = [i64, i64, vp, i64, vp, i64, vp]
+    L.tm_blur_dist.argtypes = [vp, i64, i64, vp, i64, vp, i64, vp]
+    L.tm_blur_dist_loopback.argtypes = [ci, i64, i64, vp, i64, vp, i64, vp, vp]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(L, name)
         if fn.restype is ctypes.c_int or name in ("tm_status_string", "tm_sgemm_plan_name"):
@@ -374,6 +377,51 @@ def sgemm_dist_loopback(m, n, k, A_locals, Bs, C_locals, alpha=1.0, beta=0.0, ro
     return [int(x) for x in got]
 
 
+def _image(name, t, rows=None, cols=None):
+    """(pointer, row pitch in floats) of an (N, M, 3) float32 CUDA image whose
+    rows may be padded (strides (ld, 3, 1))."""
+    _f32(name, t)
+    if t.dim() != 3 or t.shape[2] != 3:
+        raise ValueError(f"{name} must have shape (N, M, 3), got {tuple(t.shape)}")
+    if rows is not None and tuple(t.shape[:2]) != (rows, cols):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected ({rows}, {cols}, 3)")
+    if t.shape[1] > 0 and (t.stride(2) != 1 or (t.shape[1] > 1 and t.stride(1) != 3)):
+        raise ValueError(f"{name}: each row must be 3*M contiguous floats")
+    ld = int(t.stride(0)) if t.shape[0] > 1 else 3 * int(t.shape[1])
+    return t.data_ptr(), ld
+
+
+def blur(inp, out=None, stream=None):
+    """The paper's two-stage 3x3 blur: inp (N, M, 3) ->
+    out (N-2, M-2, 3), float32 CUDA tensors (rows may be padded)."""
+    import torch
+    N, M = int(inp.shape[0]), int(inp.shape[1])
+    if out is None:
+        out = torch.empty((N - 2, M - 2, 3), dtype=torch.float32, device=inp.device)
+    _on_device(inp=inp, out=out)
+    pi, ldi = _image("inp", inp)
+    po, ldo = _image("out", out, N - 2, M - 2)
+    _check(lib.tm_blur(N, M, pi, ldi, po, ldo, _stream(stream)), "tm_blur")
+    return out
+
+
+def blur_dist_loopback(N, M, lins, louts, stream=None):
+    """Single-process emulation of Comm.blur over len(lins) simulated ranks:
+    lins[r] (rows_r + 2, M, 3), louts[r] (rows_r, M-2, 3) with rows_r from
+    dist_rows(N-2, P, r).  Returns the bytes each simulated rank received."""
+    P = len(lins)
+    infos_i = [_image("lin", t, dist_rows(N - 2, P, r)[1] + 2, M) for r, t in enumerate(lins)]
+    infos_o = [_image("lout", t, dist_rows(N - 2, P, r)[1], M - 2) for r, t in enumerate(louts)]
+    if len({ld for _, ld in infos_i}) != 1 or len({ld for _, ld in infos_o}) != 1:
+        raise ValueError("every rank's lin (lout) must have the same row pitch")
+    arr = lambda xs: (ctypes.c_void_p * P)(*[p for p, _ in xs])
+    got = (ctypes.c_uint64 * P)()
+    st = lib.tm_blur_dist_loopback(P, N, M, arr(infos_i), infos_i[0][1], arr(infos_o), infos_o[0][1], got,
+                                   _stream(stream))
+    _check(st, "tm_blur_dist_loopback")
+    return [int(x) for x in got]
+
+
 def unique_id() -> bytes:
     """A fresh NCCL unique id (host-only)."""
     uid = (ctypes.c_ubyte * 128)()
@@ -449,3 +497,14 @@ class Comm:
                                          _ld(C_local) if C_local.shape[0] > 0 else max(n, 1), _stream(stream))
         _check(st, "tm_sgemm_dist_allgather")
         return C_local
+
+    def blur(self, N, M, lin, lout, stream=None):
+        """Row-distributed blur: lin (rows + 2, M, 3) holds
+        this rank's input rows plus the 2-row border region (received from rank
+        r+1; the last rank supplies input rows N-2, N-1 there), lout (rows, M-2, 3);
+        rows from dist_rows(N-2, P, rank)."""
+        rows = dist_rows(N - 2, self.nranks, self.rank)[1]
+        pi, ldi = _image("lin", lin, rows + 2, M)
+        po, ldo = _image("lout", lout, rows, M - 2)
+        _check(lib.tm_blur_dist(self.handle, N, M, pi, ldi, po, ldo, _stream(stream)), "tm_blur_dist")
+        return lout

@@ -247,6 +247,13 @@ std::vector<void*> g_sk_retired;
 
 }  // namespace
 
+tm_status device_sms(int* sms) {
+  DevInfo* d = nullptr;
+  tm_status st = current_device(&d);
+  if (st == TM_OK && sms) *sms = d->sms;
+  return st;
+}
+
 bool tc_plan_ok(const GemmArgs& a) { return make_plan(a, TM_ALGO_TF32X3, 148).path == Path::kTc; }
 
 tm_status sgemm_reserve(const GemmArgs& a, cudaStream_t stream, int sm_reserve) {

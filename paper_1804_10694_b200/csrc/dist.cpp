@@ -70,6 +70,11 @@ struct Nccl {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  // point-to-point (the blur's border-row exchange)
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   bool ok = false;
 };
 
@@ -95,6 +100,10 @@ void load_nccl() {
   g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
   g_nccl.Broadcast = reinterpret_cast<decltype(g_nccl.Broadcast)>(dlsym(h, "ncclBroadcast"));
   g_nccl.AllGather = reinterpret_cast<decltype(g_nccl.AllGather)>(dlsym(h, "ncclAllGather"));
+  g_nccl.Send = reinterpret_cast<decltype(g_nccl.Send)>(dlsym(h, "ncclSend"));
+  g_nccl.Recv = reinterpret_cast<decltype(g_nccl.Recv)>(dlsym(h, "ncclRecv"));
+  g_nccl.GroupStart = reinterpret_cast<decltype(g_nccl.GroupStart)>(dlsym(h, "ncclGroupStart"));
+  g_nccl.GroupEnd = reinterpret_cast<decltype(g_nccl.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
   g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.Broadcast && g_nccl.AllGather;
 }
 
@@ -467,6 +476,57 @@ tm_status allgather_schedule(int nranks, int rank, int64_t m, int64_t n, int64_t
   return TM_OK;
 }
 
+// Row-distributed blur (Fig. 5 Code 3).  Rank r owns
+// output rows [row0, row0 + rows) of the N-2 (tm_dist_rows(N-2, P, r)) and the
+// matching input rows in lin[0, rows); the two border rows lin[rows, rows + 2)
+// come from rank r+1 (its lin[0, 2)), the last rank's are the caller's.
+// `exchange(send_buf, recv_buf, count)` enqueues on comm_stream the send of
+// this rank's first two rows to r-1 (send_buf null on rank 0) and the receive
+// of r+1's into the border region (recv_buf null on the last rank).  The
+// interior rows [0, rows - 2) need no border and run while it is in flight.
+template <class Exchange>
+tm_status blur_dist_schedule(int nranks, int rank, int64_t N, int64_t M, float* lin, int64_t ldi, float* lout,
+                             int64_t ldo, cudaStream_t stream, cudaStream_t comm_stream, cudaEvent_t ev_start,
+                             cudaEvent_t ev_halo, uint64_t* bytes_received, Exchange&& exchange) {
+  if (N < 3 || M < 3 || ldi < 3 * M || ldo < 3 * (M - 2) || !lin || !lout) return TM_ERR_INVALID_VALUE;
+  if (nranks > 1 && (N - 2) / nranks < 2) return TM_ERR_INVALID_VALUE;
+  int64_t row0 = 0, rows = 0;
+  tm_dist_rows(N - 2, nranks, rank, &row0, &rows);
+  {  // lout must not overlap lin (rows + 2 input rows)
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(lin), o0 = reinterpret_cast<uintptr_t>(lout);
+    const uintptr_t ib = static_cast<uintptr_t>(((rows + 1) * ldi + 3 * M) * 4);
+    const uintptr_t ob = static_cast<uintptr_t>(((rows - 1) * ldo + 3 * (M - 2)) * 4);
+    if (i0 < o0 + ob && o0 < i0 + ib) return TM_ERR_INVALID_VALUE;
+  }
+  int sms = 0;
+  tm_status st = tmk::device_sms(&sms);
+  if (st != TM_OK) return st;
+  const bool last = rank == nranks - 1;
+  if (nranks == 1 || (last && rank == 0))
+    return tmk::launch_blur(0, rows, M, lin, ldi, lout, ldo, sms, stream);
+  // two rows of the paper's M*2*3 contiguous elements, here row pitch ldi
+  const size_t count = static_cast<size_t>(ldi + 3 * M);
+  if (cudaEventRecord(ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (cudaStreamWaitEvent(comm_stream, ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
+  nvtxRangePushA("tm_blur_dist schedule");
+  struct Pop {
+    ~Pop() { nvtxRangePop(); }
+  } pop;
+  st = exchange(rank > 0 ? lin : nullptr, last ? nullptr : lin + rows * ldi, count);
+  if (st != TM_OK) return st;
+  if (!last && bytes_received) *bytes_received += count * 4;
+  if (cudaEventRecord(ev_halo, comm_stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (last) {  // border rows are local: one launch, then join the send
+    st = tmk::launch_blur(0, rows, M, lin, ldi, lout, ldo, sms, stream);
+    if (st != TM_OK) return st;
+    return cudaStreamWaitEvent(stream, ev_halo, 0) == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+  }
+  st = tmk::launch_blur(0, rows - 2, M, lin, ldi, lout, ldo, sms, stream);  // interior, overlaps the exchange
+  if (st != TM_OK) return st;
+  if (cudaStreamWaitEvent(stream, ev_halo, 0) != cudaSuccess) return TM_ERR_CUDA;
+  return tmk::launch_blur(rows - 2, rows, M, lin, ldi, lout, ldo, sms, stream);
+}
+
 }  // namespace
 
 extern "C" {
@@ -593,6 +653,56 @@ tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t 
   return allgather_schedule(comm->nranks, comm->rank, m, n, k, alpha, A_local, lda, B_shard, B_full, ldb, beta,
                             C_local, ldc, static_cast<cudaStream_t>(stream_), comm->stream, comm->ev_start,
                             comm->ev_chunk[0], &comm->bytes_received, gather);
+}
+
+tm_status tm_blur_dist(tm_comm_t comm, int64_t N, int64_t M, float* lin, int64_t ldi, float* lout, int64_t ldo,
+                       void* stream_) {
+  if (!comm) return TM_ERR_INVALID_VALUE;
+  if (comm->nranks > 1 && !(g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd)) return TM_ERR_NCCL;
+  const int r = comm->rank;
+  auto exchange = [&](const float* send_buf, float* recv_buf, size_t count) -> tm_status {
+    if (g_nccl.GroupStart() != ncclSuccess) return TM_ERR_NCCL;
+    bool ok = true;
+    if (send_buf) ok = g_nccl.Send(send_buf, count, ncclFloat32, r - 1, comm->comm, comm->stream) == ncclSuccess;
+    if (ok && recv_buf) ok = g_nccl.Recv(recv_buf, count, ncclFloat32, r + 1, comm->comm, comm->stream) == ncclSuccess;
+    const bool ended = g_nccl.GroupEnd() == ncclSuccess;
+    return ok && ended ? TM_OK : TM_ERR_NCCL;
+  };
+  return blur_dist_schedule(comm->nranks, r, N, M, lin, ldi, lout, ldo, static_cast<cudaStream_t>(stream_),
+                            comm->stream, comm->ev_start, comm->ev_chunk[0], &comm->bytes_received, exchange);
+}
+
+tm_status tm_blur_dist_loopback(int nranks, int64_t N, int64_t M, float* const* lins, int64_t ldi,
+                                float* const* louts, int64_t ldo, uint64_t* bytes_received, void* stream_) {
+  if (nranks < 1 || !lins || !louts) return TM_ERR_INVALID_VALUE;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_halo = nullptr;
+  tm_status st = TM_OK;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ev_halo, cudaEventDisableTiming) != cudaSuccess)
+    st = TM_ERR_CUDA;
+  if (bytes_received)
+    for (int r = 0; r < nranks; ++r) bytes_received[r] = 0;
+  // Ranks one after another; rank r's receive copies rank r+1's first two rows
+  // (its send is the matching receive of rank r-1, so it moves nothing here).
+  for (int r = 0; st == TM_OK && r < nranks; ++r) {
+    auto exchange = [&](const float*, float* recv_buf, size_t count) -> tm_status {
+      if (!recv_buf) return TM_OK;
+      return cudaMemcpyAsync(recv_buf, lins[r + 1], count * 4, cudaMemcpyDeviceToDevice, cs) == cudaSuccess
+                 ? TM_OK
+                 : TM_ERR_CUDA;
+    };
+    st = blur_dist_schedule(nranks, r, N, M, lins[r], ldi, louts[r], ldo, stream, cs, ev_start, ev_halo,
+                            bytes_received ? &bytes_received[r] : nullptr, exchange);
+    if (st == TM_OK && cudaStreamSynchronize(stream) != cudaSuccess) st = TM_ERR_CUDA;
+  }
+  if (cs) cudaStreamSynchronize(cs);
+  if (ev_halo) cudaEventDestroy(ev_halo);
+  if (ev_start) cudaEventDestroy(ev_start);
+  if (cs) cudaStreamDestroy(cs);
+  return st;
 }
 
 }  // extern "C"

@@ -25,6 +25,10 @@ tm_status ensure_smem_optin(std::atomic<unsigned long long>& done, Kernel kern, 
   return TM_OK;
 }
 
+// The current device's SM count, after checking it is an sm_100 part
+// (TM_ERR_UNSUPPORTED_DEVICE otherwise; api.cpp).
+tm_status device_sms(int* sms);
+
 // C = alpha * op(A) * op(B) + beta * C, row-major.  ta: op(A) = A^T (A stored
 // k x m, lda >= m); tb: op(B) = B^T (B stored n x k, ldb >= k).
 struct GemmArgs {
@@ -114,6 +118,12 @@ tm_status launch_conv_direct(const ConvArgs& a, int num_sms, cudaStream_t stream
 bool tune_lookup(const GemmArgs& a, int sms, TcChoice* out);
 // Whether tm_sgemm_op(..., TM_ALGO_TF32X3) would accept these arguments (host-only).
 bool tc_plan_ok(const GemmArgs& a);
+
+// Blur (blur.cu): output rows [i0, i1) of the two-stage
+// 3x3 box blur of an image with N rows of 3M floats (pitch ldi), into out rows
+// [i0, i1) (pitch ldo).  The rows needed from `in` are [i0, i1 + 2).
+tm_status launch_blur(int64_t i0, int64_t i1, int64_t M, const float* in, int64_t ldi, float* out, int64_t ldo,
+                      int num_sms, cudaStream_t stream);
 
 // Picks the tensor-core configuration for a shape (planner, plan.cpp).
 TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms);

@@ -110,3 +110,15 @@ def sample_rows(m: int, count: int = 256, seed: int = 7, tile: int = 128, extra=
     while len(rows) < min(count, m):
         rows = sorted(set(rows) | {int(g.integers(0, m))})
     return np.asarray(rows, dtype=np.int64)
+
+
+# The paper's image-processing input ("a 2112x3520 RGB input
+# image"): the Blur workload runs on it.
+BLUR_IMAGE = (2112, 3520)
+BLUR_SEED = 1842
+
+
+def image(N: int, M: int, seed: int = BLUR_SEED, signed: bool = False) -> np.ndarray:
+    """N x M x 3 float32 RGB image, channels interleaved (the paper's in[i][j][c]):
+    pixel intensities U[0, 1) (or U[-1, 1) with signed=True, a cancellation stress)."""
+    return uniform(rng(seed), (N, M, 3), -1.0 if signed else 0.0, 1.0)

@@ -170,3 +170,24 @@ def test_binding_rejects_mismatched_shapes_and_host_tensors():
         tm.sgemm_host(A.numpy(), Bs, C.numpy())
     with pytest.raises(ValueError):
         tm.sgemm_host(A.numpy(), np.zeros((4, 6), np.float32)[::-1], C.numpy())  # negative row stride
+
+
+@pytest.mark.parametrize("args", [
+    dict(N=2, M=5),                      # fewer than 3 rows: no output of the 3x3 stencil
+    dict(N=5, M=2),                      # fewer than 3 columns
+    dict(N=5, M=5, ldi=14),              # ldi < 3M
+    dict(N=5, M=5, ldo=8),               # ldo < 3(M-2)
+    dict(N=5, M=5, inp=0),               # NULL in
+    dict(N=5, M=5, out=0),               # NULL out
+    dict(N=5, M=5, out=(1 << 20) + 40),  # out overlaps in
+])
+def test_blur_invalid_arguments_rejected_on_host(args):
+    N, M = args["N"], args["M"]
+    st = tm.lib.tm_blur(N, M, ctypes.c_void_p(args.get("inp", 1 << 20)), args.get("ldi", 3 * M),
+                        ctypes.c_void_p(args.get("out", 1 << 24)), args.get("ldo", 3 * max(M - 2, 1)), None)
+    assert st == 1
+
+
+def test_blur_dist_loopback_rejects_bad_rank_count_on_host():
+    P = (ctypes.c_void_p * 1)(1 << 20)
+    assert tm.lib.tm_blur_dist_loopback(0, 9, 9, P, 27, P, 21, None, None) == 1
