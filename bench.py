@@ -409,7 +409,7 @@ def main():
             clk_peak = 148 * (8192 if kernel == "bf16x9" else 4096) * f_sm * 1e6 / 1e12 / per_product
             roof["frac_clock_normalized"] = round(achieved / clk_peak, 4)
             roof["clock_normalized_peak"] = round(clk_peak, 2)
-    launches = args.steps * (1 if comm is None else max(1, min(8, k // 512)))
+    launches = args.steps * (1 if comm is None else len(tm.dist_chunks(k, world)))
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,

@@ -330,6 +330,59 @@ tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t 
                                   int64_t ldc, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Copy-engine chain broadcast (the paper's explicit
+ * send/receive between row-owning ranks).
+ *
+ * Same result as tm_sgemm_dist, but B travels root -> root+1 -> ... as a
+ * pipelined chain of device-to-device copies into the successor's buffer
+ * through CUDA IPC mappings -- executed by the copy engines, so the GEMM keeps
+ * every SM (tm_sgemm_dist leaves 16 to NCCL's kernels).  Each 256-K-row piece
+ * is flagged on arrival with a stream memory operation; a rank gives its
+ * predecessor a credit (its B is free) at the start of every call.
+ *
+ * Bootstrap (no NCCL): every rank calls tm_ce_create, all-gathers the
+ * exported flag handles (any host transport, e.g. torch.distributed), then
+ * tm_ce_connect.  Every call passes the all-gathered tm_ipc_export of each
+ * rank's B buffer (re-export when a buffer changes).  Device memory must come
+ * from cudaMalloc (or torch's default caching allocator); one process per
+ * device, or several processes sharing a device (the tests do).
+ * ------------------------------------------------------------------------- */
+typedef struct { unsigned char bytes[64]; int64_t offset; } tm_ipc_buf; /* IPC handle of the allocation + byte offset */
+typedef struct tm_ce_s* tm_ce_t;
+
+/* Exports the allocation containing the device pointer `ptr` (cudaIpcGetMemHandle
+ * of its base) and ptr's offset in it.  TM_ERR_INVALID_VALUE if ptr is not
+ * device memory of this process, TM_ERR_CUDA if the allocation cannot be
+ * exported (e.g. virtual-memory-API allocations). */
+tm_status tm_ipc_export(const void* ptr, tm_ipc_buf* out);
+
+/* Creates this rank's chain endpoint on the CURRENT device (its flag array,
+ * two streams, events) and exports the flags in *my_flags. */
+tm_status tm_ce_create(tm_ce_t* out, int nranks, int rank, tm_ipc_buf* my_flags);
+/* Maps every peer's flags (all_flags: nranks entries, all-gathered from
+ * tm_ce_create).  Collective in the sense that all ranks must call it before
+ * the first tm_sgemm_dist_ce. */
+tm_status tm_ce_connect(tm_ce_t ce, const tm_ipc_buf* all_flags);
+/* Synchronises the endpoint's streams, unmaps peers and frees it. */
+tm_status tm_ce_destroy(tm_ce_t ce);
+/* Bytes of B this rank received through the chain since tm_ce_create. */
+tm_status tm_ce_bytes_received(tm_ce_t ce, uint64_t* bytes);
+
+/* Collective: all ranks call with identical m, n, k, alpha, beta, root, fused,
+ * in the same order.  Arguments as tm_sgemm_dist (B: a k*ldb device buffer on
+ * every rank, valid on root, overwritten elsewhere; whole rows move), plus
+ * all_B: nranks tm_ipc_export records of every rank's B.  fused != 0: one
+ * flag-gated GEMM over the full K (tm_sgemm_dist_fused's kernel, gated per
+ * piece); 0: the K-chunked schedule with every SM.  Stream-ordered; on return
+ * (stream-ordered) C_local = alpha*A_local*B + beta*C_local and B is complete.
+ * A peer that never makes its call leaves this rank's streams waiting (no
+ * timeout in the copy chain; the fused GEMM traps after ~20 s). */
+tm_status tm_sgemm_dist_ce(tm_ce_t ce, int64_t m, int64_t n, int64_t k, float alpha,
+                           const float* A_local, int64_t lda, float* B, int64_t ldb,
+                           const tm_ipc_buf* all_B, int root, float beta, float* C_local,
+                           int64_t ldc, int fused, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Blur: the paper's second distributed workload.
  *
  * The two-stage 3x3 box blur of PAPER.md:216-219 (Fig. 3):

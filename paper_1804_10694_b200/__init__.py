@@ -16,7 +16,7 @@ import os
 __all__ = [
     "ALGO_AUTO", "ALGO_TF32X3", "ALGO_SIMT_F32", "ALGO_TF32X1", "ALGO_BF16X9", "TmError", "lib", "lib_path", "sgemm",
     "sgemm_ex", "sgemm_host", "plan_name", "plan_config", "tune", "tune_cache_save", "tune_cache_load",
-    "tune_cache_clear", "tune_cache_size", "dist_rows", "Comm", "blur", "blur_dist_loopback", "status_string", "EXPORTED_SYMBOLS",
+    "tune_cache_clear", "tune_cache_size", "dist_rows", "Comm", "CeComm", "blur", "blur_dist_loopback", "status_string", "EXPORTED_SYMBOLS",
 ]
 
 ALGO_AUTO, ALGO_TF32X3, ALGO_SIMT_F32, ALGO_TF32X1, ALGO_BF16X9 = 0, 1, 2, 3, 4
@@ -31,6 +31,7 @@ EXPORTED_SYMBOLS = [
     "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_fused", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
     "tm_sgemm_tune", "tm_tune_cache_size", "tm_tune_cache_clear", "tm_tune_cache_save", "tm_tune_cache_load",
     "tm_sgemm_plan_config", "tm_blur", "tm_blur_dist", "tm_blur_dist_loopback",
+    "tm_ipc_export", "tm_ce_create", "tm_ce_connect", "tm_ce_destroy", "tm_ce_bytes_received", "tm_sgemm_dist_ce",
 ]
 
 
@@ -80,6 +81,12 @@ def _load():
     L.tm_blur.argtypes = [i64, i64, vp, i64, vp, i64, vp]
     L.tm_blur_dist.argtypes = [vp, i64, i64, vp, i64, vp, i64, vp]
     L.tm_blur_dist_loopback.argtypes = [ci, i64, i64, vp, i64, vp, i64, vp, vp]
+    L.tm_ipc_export.argtypes = [vp, vp]
+    L.tm_ce_create.argtypes = [ctypes.POINTER(vp), ci, ci, vp]
+    L.tm_ce_connect.argtypes = [vp, vp]
+    L.tm_ce_destroy.argtypes = [vp]
+    L.tm_ce_bytes_received.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+    L.tm_sgemm_dist_ce.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, i64, vp, ci, f32, vp, i64, ci, vp]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(L, name)
         if fn.restype is ctypes.c_int or name in ("tm_status_string", "tm_sgemm_plan_name"):
@@ -420,6 +427,87 @@ def blur_dist_loopback(N, M, lins, louts, stream=None):
                                    _stream(stream))
     _check(st, "tm_blur_dist_loopback")
     return [int(x) for x in got]
+
+
+class IpcBuf(ctypes.Structure):
+    """tm_ipc_buf: CUDA IPC handle of an allocation + byte offset (tm.h)."""
+    _fields_ = [("bytes", ctypes.c_ubyte * 64), ("offset", ctypes.c_int64)]
+
+
+def ipc_export(t) -> bytes:
+    """72 bytes (tm_ipc_buf) naming the device buffer of tensor t for other processes."""
+    b = IpcBuf()
+    _check(lib.tm_ipc_export(ctypes.c_void_p(t.data_ptr()), ctypes.byref(b)), "tm_ipc_export")
+    return ctypes.string_at(ctypes.addressof(b), ctypes.sizeof(b))
+
+
+def _ipc_array(blobs):
+    arr = (IpcBuf * len(blobs))()
+    for i, blob in enumerate(blobs):
+        ctypes.memmove(ctypes.addressof(arr[i]), blob, ctypes.sizeof(IpcBuf))
+    return arr
+
+
+class CeComm:
+    """Copy-engine chain endpoint (tm_ce_*): B broadcast by copy engines over
+    CUDA IPC mappings, no NCCL and no SMs taken from the GEMM.  Bootstrap and
+    buffer-handle exchange go through a torch.distributed group (any backend)."""
+
+    def __init__(self, rank: int, nranks: int, group=None):
+        import torch.distributed as dist
+        self.rank, self.nranks, self.group = rank, nranks, group
+        h, fl = ctypes.c_void_p(), IpcBuf()
+        _check(lib.tm_ce_create(ctypes.byref(h), nranks, rank, ctypes.byref(fl)), "tm_ce_create")
+        self.handle = h
+        blobs = [ctypes.string_at(ctypes.addressof(fl), ctypes.sizeof(fl))]
+        if nranks > 1:
+            allb = [None] * nranks
+            dist.all_gather_object(allb, blobs[0], group=group)
+            blobs = allb
+        self._flags = _ipc_array(blobs)
+        _check(lib.tm_ce_connect(self.handle, self._flags), "tm_ce_connect")
+
+    def exchange(self, B):
+        """All ranks' tm_ipc_export of their B buffers (collective): pass to sgemm
+        as `handles`; valid while every rank keeps the same buffer."""
+        import torch.distributed as dist
+        mine = ipc_export(B)
+        if self.nranks == 1:
+            return _ipc_array([mine])
+        allb = [None] * self.nranks
+        dist.all_gather_object(allb, mine, group=self.group)
+        return _ipc_array(allb)
+
+    def sgemm(self, m, n, k, A_local, B, C_local, alpha=1.0, beta=0.0, root=0, stream=None, fused=False,
+              handles=None):
+        """Row-sharded C_local <- alpha*A_local@B + beta*C_local, B chain-broadcast
+        from root by copy engines (tm_sgemm_dist_ce).  B: a dense k*ldb buffer on
+        every rank.  handles: from exchange(B) (done here when None)."""
+        if handles is None:
+            handles = self.exchange(B)
+        st = lib.tm_sgemm_dist_ce(self.handle, m, n, k, float(alpha), _ptr(A_local),
+                                  _ld(A_local) if A_local is not None and A_local.shape[0] > 0 else max(k, 1),
+                                  _ptr(B), _ld(B), handles, int(root), float(beta), _ptr(C_local),
+                                  _ld(C_local) if C_local.shape[0] > 0 else max(n, 1), int(bool(fused)),
+                                  _stream(stream))
+        _check(st, "tm_sgemm_dist_ce")
+        return C_local
+
+    def bytes_received(self) -> int:
+        v = ctypes.c_uint64()
+        _check(lib.tm_ce_bytes_received(self.handle, ctypes.byref(v)), "tm_ce_bytes_received")
+        return int(v.value)
+
+    def close(self):
+        if self.handle:
+            _check(lib.tm_ce_destroy(self.handle), "tm_ce_destroy")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def unique_id() -> bytes:

@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libtm.so")
 STAMP = LIB + ".build.json"  # source hash + the exact nvcc commands of the build that produced LIB
-SOURCES = ["api.cpp", "plan.cpp", "dist.cpp", "tune.cpp", "simt_gemm.cu", "small_gemm.cu", "tc_gemm_nn.cu", "tc_gemm_nt.cu", "tc_gemm_tn.cu", "tc_gemm_tt.cu", "tc_conv.cu", "tc_conv_direct.cu", "blur.cu"]
+SOURCES = ["api.cpp", "plan.cpp", "dist.cpp", "tune.cpp", "simt_gemm.cu", "small_gemm.cu", "tc_gemm_nn.cu", "tc_gemm_nt.cu", "tc_gemm_tn.cu", "tc_gemm_tt.cu", "tc_conv.cu", "tc_conv_direct.cu", "blur.cu", "ce_chain.cpp"]
 HEADERS = ["ptx.cuh", "tm_internal.h", "tc_gemm.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -114,28 +114,7 @@ bool nccl() {
 
 constexpr int kMaxChunks = 16;
 
-// cuStreamWriteValue32 through the runtime's driver entry-point query (no
-// link-time libcuda dependency): the transfer stream publishes "chunk c has
-// arrived" with a stream memory operation (no kernel, no SM), ordered after the
-// chunk's transfer on that stream.
-using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-WriteValue32Fn write_value32() {
-  static WriteValue32Fn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      return reinterpret_cast<WriteValue32Fn>(p);
-    return static_cast<WriteValue32Fn>(nullptr);
-  }();
-  return fn;
-}
-tm_status set_flag(cudaStream_t s, unsigned* flag, unsigned value) {
-  WriteValue32Fn fn = write_value32();
-  if (!fn) return TM_ERR_CUDA;
-  return fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0) == CUDA_SUCCESS ? TM_OK
-                                                                                                    : TM_ERR_CUDA;
-}
+tm_status set_flag(cudaStream_t s, unsigned* flag, unsigned value) { return tmk::stream_write_u32(s, flag, value); }
 
 // Loopback link model (projection only, TM_LOOPBACK_LINK_GBS): after each
 // chunk's on-device copy the transfer stream spins for bytes / rate, so the
@@ -166,6 +145,57 @@ double loopback_link_gbs() {
 }
 
 }  // namespace
+
+namespace tmk {
+
+// Stream memory operations through the runtime's driver entry-point query (no
+// link-time libcuda dependency): no kernel, no SM; ordered in the stream like
+// any other operation (the write after all earlier work, with a memory barrier).
+namespace {
+template <class Fn>
+Fn driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<Fn>(p);
+  return nullptr;
+}
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using AddressRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+}  // namespace
+
+tm_status stream_write_u32(cudaStream_t s, unsigned* flag, unsigned value) {
+  static const WriteValue32Fn fn = driver_fn<WriteValue32Fn>("cuStreamWriteValue32");
+  if (!fn) return TM_ERR_CUDA;
+  return fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0) == CUDA_SUCCESS
+             ? TM_OK
+             : TM_ERR_CUDA;
+}
+
+tm_status stream_wait_u32(cudaStream_t s, const unsigned* flag, unsigned value) {
+  static const WaitValue32Fn fn = driver_fn<WaitValue32Fn>("cuStreamWaitValue32");
+  if (!fn) return TM_ERR_CUDA;
+  // CU_STREAM_WAIT_VALUE_GEQ (0): until (int32)(*flag - value) >= 0 -- epochs wrap safely
+  return fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), value, 0) == CUDA_SUCCESS
+             ? TM_OK
+             : TM_ERR_CUDA;
+}
+
+tm_status device_allocation(const void* p, void** base, size_t* bytes) {
+  static const AddressRangeFn fn = driver_fn<AddressRangeFn>("cuMemGetAddressRange");
+  if (!fn) return TM_ERR_CUDA;
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return TM_ERR_INVALID_VALUE;
+  *base = reinterpret_cast<void*>(b);
+  if (bytes) *bytes = sz;
+  return TM_OK;
+}
+
+int dist_comm_ctas() { return comm_ctas(); }
+
+}  // namespace tmk
 
 struct tm_comm_s {
   ncclComm_t comm = nullptr;
@@ -279,27 +309,77 @@ tm_status tm_comm_bytes_received(tm_comm_t c, uint64_t* bytes) {
 
 static int choose_chunks(int64_t k, int nranks) {
   if (nranks <= 1) return 1;
-  // Chunks of at least 512 K-rows; at most 8 (the first chunk is the exposed
-  // transfer, later ones hide behind the previous chunk's GEMM).
+  // Uniform chunks (the fused schedule's flag granularity): at least 512
+  // K-rows; at most 8.
   int64_t c = k / 512;
   if (c > 8) c = 8;
   if (c < 1) c = 1;
   return static_cast<int>(c);
 }
 
-tm_status tm_dist_chunk(int64_t k, int nranks, int idx, int64_t* k0, int64_t* kr) {
-  if (k < 0 || nranks < 1 || !k0 || !kr) return TM_ERR_INVALID_VALUE;
+// Uniform plan: nch chunks of kc rows (multiple of 32), the last ragged.
+static int uniform_plan(int64_t k, int nranks, int64_t* bounds) {
   const int nch = choose_chunks(k, nranks);
   const int64_t kc = ((k + nch - 1) / nch + 31) / 32 * 32;
-  const int64_t count = k == 0 ? 0 : (k + kc - 1) / kc;
+  int n = 0;
+  bounds[0] = 0;
+  for (int64_t k0 = 0; k0 < k; k0 += kc) bounds[++n] = std::min(k, k0 + kc);
+  return n;
+}
+
+// The chunked schedule's K-chunks: geometric, each twice the previous,
+// starting at max(512, k/32) rows (multiples of 32); a remainder of at most
+// half the last chunk is merged into it, a larger one becomes its own chunk.
+// Rationale: chunk 0 is the exposed transfer, so it is
+// small; chunk c+1 arrives while chunk c's GEMM runs as long as the link moves
+// a K-row faster than the GEMM consumes it divided by the growth factor (at
+// 16384^3 / P = 8: 0.26 us of GEMM vs 0.09 us of NVLink per K-row, margin
+// 1.4x), and every chunk boundary costs a launch tail and a round trip of C,
+// so few, growing chunks beat many uniform ones.  TM_DIST_CHUNKS=uniform
+// selects the uniform plan (measurement knob).
+static int chunk_plan(int64_t k, int nranks, int64_t* bounds) {
+  bounds[0] = 0;
+  if (k <= 0) return 0;
+  if (nranks <= 1) {
+    bounds[1] = k;
+    return 1;
+  }
+  static const bool uniform = [] {
+    const char* e = std::getenv("TM_DIST_CHUNKS");
+    return e && std::strcmp(e, "uniform") == 0;
+  }();
+  if (uniform) return uniform_plan(k, nranks, bounds);
+  int64_t s = std::max<int64_t>(512, (k / 32 + 31) / 32 * 32);
+  int n = 0;
+  int64_t sum = 0;
+  while (n < kMaxChunks && sum + s <= k) {
+    sum += s;
+    bounds[++n] = sum;
+    s *= 2;
+  }
+  const int64_t rest = k - sum;
+  if (n == 0) {
+    bounds[++n] = k;
+  } else if (rest > 0) {
+    const int64_t last = bounds[n] - bounds[n - 1];
+    if (rest * 2 > last && n < kMaxChunks) bounds[++n] = k;
+    else bounds[n] = k;
+  }
+  return n;
+}
+
+tm_status tm_dist_chunk(int64_t k, int nranks, int idx, int64_t* k0, int64_t* kr) {
+  if (k < 0 || nranks < 1 || !k0 || !kr) return TM_ERR_INVALID_VALUE;
+  int64_t bounds[kMaxChunks + 1];
+  const int count = chunk_plan(k, nranks, bounds);
   if (idx < 0) {
     *k0 = count;
-    *kr = kc;
+    *kr = count ? bounds[count] - bounds[count - 1] : 0;  // the largest (last) chunk
     return TM_OK;
   }
   if (idx >= count) return TM_ERR_INVALID_VALUE;
-  *k0 = idx * kc;
-  *kr = (*k0 + kc <= k) ? kc : k - *k0;
+  *k0 = bounds[idx];
+  *kr = bounds[idx + 1] - bounds[idx];
   return TM_OK;
 }
 
@@ -316,13 +396,16 @@ namespace {
 // (no GEMM ever waits inside a kernel on the broadcast).  Rates: NVLink ~700
 // GB/s per rank, 3xTF32 GEMM ~240 TFLOP/s (measured C5; TM_DIST_LINK_GBS and
 // TM_DIST_GEMM_TFLOPS override them).
-bool chunk_overlaps_transfer(int c, int nchunks, int64_t rows, int64_t n, int64_t kc, int64_t ldb) {
+bool chunk_overlaps_transfer(const int64_t* bounds, int c, int nchunks, int64_t rows, int64_t n, int64_t ldb) {
   static const double link = [] { const char* e = std::getenv("TM_DIST_LINK_GBS"); return e ? std::atof(e) : 700.0; }();
   static const double gemm = [] { const char* e = std::getenv("TM_DIST_GEMM_TFLOPS"); return e ? std::atof(e) : 240.0; }();
   if (link <= 0.0 || gemm <= 0.0) return true;
-  const double t_xfer = 4.0 * static_cast<double>(kc) * static_cast<double>(ldb) / (link * 1e9);  // one chunk
-  const double t_gemm = 2.0 * static_cast<double>(rows) * static_cast<double>(n) * static_cast<double>(kc) / (gemm * 1e12);
-  return t_xfer + c * t_gemm < nchunks * t_xfer;
+  const double per_row_xfer = 4.0 * static_cast<double>(ldb) / (link * 1e9);
+  const double per_row_gemm = 2.0 * static_cast<double>(rows) * static_cast<double>(n) / (gemm * 1e12);
+  // chunk c's GEMM starts after chunk 0 arrived and chunks 0..c-1 computed;
+  // the broadcast ends after all of B crossed the link
+  const double start = static_cast<double>(bounds[1]) * per_row_xfer + static_cast<double>(bounds[c]) * per_row_gemm;
+  return start < static_cast<double>(bounds[nchunks]) * per_row_xfer;
 }
 
 // The per-rank schedule of the row-sharded GEMM, shared by the NCCL mode and
@@ -342,32 +425,29 @@ tm_status dist_schedule(int nranks, int rank, int root, int64_t m, int64_t n, in
     return tm_sgemm(rows, n, k, alpha, A_local, lda, B, ldb, beta, C_local, ldc, stream);
   }
   if (!B || ldb < (n > 1 ? n : 1)) return TM_ERR_INVALID_VALUE;
-  int64_t nchunks = 0, kc = 0;
-  tm_dist_chunk(k, nranks, -1, &nchunks, &kc);
-  if (nchunks > kMaxChunks) return TM_ERR_INTERNAL;
+  int64_t bounds[kMaxChunks + 1];
+  const int nchunks = chunk_plan(k, nranks, bounds);
   if (cudaEventRecord(ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
   if (cudaStreamWaitEvent(comm_stream, ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
   nvtxRangePushA("tm_sgemm_dist schedule");
   struct Pop {
     ~Pop() { nvtxRangePop(); }
   } pop;
-  int used = 0;
-  for (int64_t k0 = 0; k0 < k; k0 += kc, ++used) {
-    const int64_t kr = (k0 + kc <= k) ? kc : k - k0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t k0 = bounds[c], kr = bounds[c + 1] - bounds[c];
     // Root sends in place; the last row's padding beyond n is inside k*ldb.
     const size_t count = static_cast<size_t>(kr) * static_cast<size_t>(ldb);
     tm_status st = xfer(B + k0 * ldb, count);
     if (st != TM_OK) return st;
     if (rank != root && bytes_received) *bytes_received += count * 4;
-    if (cudaEventRecord(ev_chunk[used], comm_stream) != cudaSuccess) return TM_ERR_CUDA;
+    if (cudaEventRecord(ev_chunk[c], comm_stream) != cudaSuccess) return TM_ERR_CUDA;
   }
-  used = 0;
-  for (int64_t k0 = 0; k0 < k; k0 += kc, ++used) {
-    const int64_t kr = (k0 + kc <= k) ? kc : k - k0;
-    if (cudaStreamWaitEvent(stream, ev_chunk[used], 0) != cudaSuccess) return TM_ERR_CUDA;
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t k0 = bounds[c], kr = bounds[c + 1] - bounds[c];
+    if (cudaStreamWaitEvent(stream, ev_chunk[c], 0) != cudaSuccess) return TM_ERR_CUDA;
     if (rows > 0) {
-      tmk::GemmArgs ga{rows, n, kr, alpha, k0 == 0 ? beta : 1.0f, A_local + k0, lda, B + k0 * ldb, ldb, C_local, ldc};
-      const int reserve = chunk_overlaps_transfer(used, static_cast<int>(nchunks), rows, n, kc, ldb) ? comm_ctas() : 0;
+      tmk::GemmArgs ga{rows, n, kr, alpha, c == 0 ? beta : 1.0f, A_local + k0, lda, B + k0 * ldb, ldb, C_local, ldc};
+      const int reserve = chunk_overlaps_transfer(bounds, c, nchunks, rows, n, ldb) ? comm_ctas() : 0;
       tm_status st = tmk::sgemm_reserve(ga, stream, reserve);
       if (st != TM_OK) return st;
     }
@@ -402,9 +482,10 @@ tm_status dist_fused_schedule(int nranks, int rank, int root, int64_t m, int64_t
   if (rows > 0 && !tmk::tc_plan_ok(ga))
     return dist_schedule(nranks, rank, root, m, n, k, alpha, A_local, lda, B, ldb, beta, C_local, ldc, stream,
                          comm_stream, ev_start, ev_chunk, bytes_received, xfer);
-  int64_t nchunks = 0, kc = 0;
-  tm_dist_chunk(k, nranks, -1, &nchunks, &kc);
-  if (nchunks > kMaxChunks) return TM_ERR_INTERNAL;
+  int64_t bounds[kMaxChunks + 1];
+  const int nchunks = uniform_plan(k, nranks, bounds);  // flags cover equal chunks of kc rows
+  const int64_t kc = bounds[1];
+  (void)nchunks;
   if (cudaEventRecord(ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
   if (cudaStreamWaitEvent(comm_stream, ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
   nvtxRangePushA("tm_sgemm_dist fused schedule");

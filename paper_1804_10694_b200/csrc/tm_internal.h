@@ -119,6 +119,16 @@ bool tune_lookup(const GemmArgs& a, int sms, TcChoice* out);
 // Whether tm_sgemm_op(..., TM_ALGO_TF32X3) would accept these arguments (host-only).
 bool tc_plan_ok(const GemmArgs& a);
 
+// Stream memory operations (dist.cpp; driver entry points, no SM): write
+// *flag = value after all earlier work of `s`; make `s` wait until
+// (int32)(*flag - value) >= 0.  flag may be peer memory (IPC-mapped).
+tm_status stream_write_u32(cudaStream_t s, unsigned* flag, unsigned value);
+tm_status stream_wait_u32(cudaStream_t s, const unsigned* flag, unsigned value);
+// Base and size of the device allocation containing p (cuMemGetAddressRange).
+tm_status device_allocation(const void* p, void** base, size_t* bytes);
+// SMs the distributed schedules leave to NCCL kernels (TM_DIST_COMM_SMS).
+int dist_comm_ctas();
+
 // Blur (blur.cu): output rows [i0, i1) of the two-stage
 // 3x3 box blur of an image with N rows of 3M floats (pitch ldi), into out rows
 // [i0, i1) (pitch ldo).  The rows needed from `in` are [i0, i1 + 2).

@@ -92,6 +92,16 @@ def test_dist_host_logic_world2_gloo():
 def test_chunk_schedule_single_process():
     import paper_1804_10694_b200 as tm
     assert tm.dist_chunks(16384, 1) == [(0, 16384)]  # P == 1: no chunking (== tm_sgemm)
-    ch = tm.dist_chunks(16384, 8)
-    assert len(ch) == 8 and all(kr == 2048 for _, kr in ch)
+    # geometric chunks (dist.cpp chunk_plan): 512, 1024, 2048, 4096, then the
+    # last absorbs a remainder of at most half its size
+    assert tm.dist_chunks(16384, 8) == [(0, 512), (512, 1024), (1536, 2048), (3584, 4096), (7680, 8704)]
+    assert tm.dist_chunks(1100, 2) == [(0, 512), (512, 588)]        # larger remainder: its own chunk
+    assert tm.dist_chunks(4096, 4) == [(0, 512), (512, 1024), (1536, 2560)]
+    assert tm.dist_chunks(600, 4) == [(0, 600)]                      # below two first chunks: one
+    for k in (1, 31, 513, 1024, 5000, 65536, 1 << 20):
+        ch = tm.dist_chunks(k, 3)
+        assert ch[0][0] == 0 and sum(kr for _, kr in ch) == k and len(ch) <= 16
+        assert all(a + ka == b for (a, ka), (b, _) in zip(ch, ch[1:]))
+        assert all(k0 % 32 == 0 for k0, _ in ch)
+        assert all(kb >= ka for (_, ka), (_, kb) in zip(ch, ch[1:-1]))  # non-decreasing before the last
     assert tm.dist_chunks(0, 4) == []

@@ -44,7 +44,7 @@ def _run(P, root, m, n, k, seed, kind="uniform", ldb=None, fused=False):
 def test_loopback_shards_match_oracle(P, root, fused):
     """fused=False: K-chunked schedule (beta chain); fused=True: one GEMM per
     rank whose TMA producers wait on per-chunk flags set by the copy stream."""
-    m, n, k = 1060, 260, 1100   # uneven rows; two K-chunks of 576 and 524
+    m, n, k = 1060, 260, 1100   # uneven rows; two K-chunks of 512 and 588
     A, B, C0, parts, Cs, got, Bs = _run(P, root, m, n, k, seed=40 + P, fused=fused)
     R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0)
     for r, ((r0, rows), C) in enumerate(zip(parts, Cs)):
@@ -78,8 +78,8 @@ def test_loopback_more_ranks_than_rows():
 
 @pytest.mark.parametrize("fused", [False, True])
 def test_loopback_c5_p8_sampled_rows(fused):
-    """BASELINE.json configs[4]: 16384^3 row-sharded over 8 ranks (8 chunks of
-    2048), sampled rows incl. every shard boundary, all-positive stress data
+    """BASELINE.json configs[4]: 16384^3 row-sharded over 8 ranks (geometric
+    K-chunks 512 ... 8704; fused: 8 uniform flag chunks of 2048), sampled rows incl. every shard boundary, all-positive stress data
     (the beta chain adds 7 extra fp32 roundings per element)."""
     import torch
     import paper_1804_10694_b200 as tm

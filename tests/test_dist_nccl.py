@@ -59,6 +59,16 @@ def test_one_rank_comm_lifecycle_and_sgemm():
         assert torch.equal(B_full, dB)
         assert _err(dC2.cpu().numpy(), R, D) <= TOL
         assert comm.bytes_received() == 0  # nothing arrives from other ranks
+        # the row-distributed blur at P = 1 is tm_blur on the whole image
+        N, M = 67, 45
+        img = si.image(N, M, seed=64)
+        lin = torch.from_numpy(img).cuda()
+        lout = torch.full((N - 2, M - 2, 3), float("nan"), device="cuda")
+        comm.blur(N, M, lin, lout)
+        ref = tm.blur(lin)
+        torch.cuda.synchronize()
+        assert torch.equal(lout, ref)
+        assert comm.bytes_received() == 0
         assert comm.check()
     finally:
         comm.close()
@@ -122,6 +132,23 @@ def _worker(rank, world, port, q):
         out["ag_B_equal"] = bool(np.array_equal(B_full.cpu().numpy(), B2))
         out["ag_bytes"] = comm.bytes_received() - before
         out["ag_bytes_expected"] = (world - 1) * kr * n * 4
+        # row-distributed blur: border rows from rank + 1 over NCCL
+        N, M = 2112, 3520 // 8
+        img = si.image(N, M, seed=65)
+        b0, brows = tm.dist_rows(N - 2, world, rank)
+        lin = torch.full((brows + 2, M, 3), float("nan"), device="cuda")
+        lin[:brows] = torch.from_numpy(img[b0:b0 + brows]).cuda()
+        if rank == world - 1:
+            lin[brows:] = torch.from_numpy(img[N - 2:]).cuda()
+        lout = torch.full((brows, M - 2, 3), float("nan"), device="cuda")
+        before = comm.bytes_received()
+        comm.blur(N, M, lin, lout)
+        torch.cuda.synchronize()
+        Rb, Db = oracle.blur(img, rows=np.arange(b0, b0 + brows))
+        got = lout.cpu().numpy().astype(np.float64)
+        out["blur_err"] = float(np.max(np.abs(got - Rb) / Db))
+        out["blur_bytes"] = comm.bytes_received() - before
+        out["blur_bytes_expected"] = 0 if rank == world - 1 else 2 * 3 * M * 4
         out["check"] = comm.check()
         comm.close()
     except Exception as e:  # reported to the parent, which fails the test
@@ -154,4 +181,5 @@ def test_multi_rank_nccl_broadcast_and_allgather():
         assert o["fused_err"] <= TOL, o
         assert o["bcast_bytes"] == o["bcast_bytes_expected"], o
         assert o["ag_bytes"] == o["ag_bytes_expected"], o
+        assert o["blur_err"] <= 1e-6 and o["blur_bytes"] == o["blur_bytes_expected"], o
         assert o["check"], o
