@@ -303,10 +303,21 @@ tm_status tm_sgemm_dist_fused(tm_comm_t comm, int64_t m, int64_t n, int64_t k, f
  *   mode 1: tm_sgemm_dist_allgather -- Bs[r] holds rank r's k-row shard at rows
  *           [r*k/P, (r+1)*k/P) (k % nranks == 0); every Bs[r] ends complete.
  *   mode 2: tm_sgemm_dist_fused -- as mode 0, with one flag-gated GEMM per
- *           rank; the chunk copies (copy-engine transport, no SMs) and the
- *           flag writes run on a separate stream concurrently with it.
- *   Env TM_LOOPBACK_LINK_GBS (projections only): each chunk additionally takes
- *   bytes / rate on the transfer stream, modelling a link of that rate.
+ *           rank; the chunk copies and the flag writes run on a separate
+ *           stream concurrently with it.
+ *   mode 3, 4: modes 0 and 2 under the copy-engine transport model
+ *           (tm_sgemm_dist_ce between devices: peer copies run on the copy
+ *           engines, which one device cannot emulate -- its own device-to-
+ *           device copies are kernels): NO data moves, the caller fills every
+ *           Bs[r] with B beforehand; chunk c is only released on the link
+ *           model's schedule (rate TM_LOOPBACK_LINK_GBS, default 700 GB/s) and
+ *           the GEMMs keep every SM but one (the pacing kernel's).  Timing
+ *           projections; the result is still checked by the tests.
+ *   Env TM_LOOPBACK_LINK_GBS = R (projections): chunk c of the rank at chain
+ *   position q (root 0) is released no earlier than (q * 128 K-rows + bytes
+ *   of chunks 0..c) / R after the rank's transfers start, modelling a
+ *   pipelined chain (or ring) of links of rate R; in modes 0-2 also no
+ *   earlier than its device copy completes.
  *   A_locals[r], Bs[r], C_locals[r]: device pointers (host arrays of nranks),
  *   shaped as the NCCL entry's A_local, B / B_full, C_local for rank r.
  *   bytes_received: optional host array of nranks counters (bytes each rank's
@@ -336,7 +347,7 @@ tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t 
  * Same result as tm_sgemm_dist, but B travels root -> root+1 -> ... as a
  * pipelined chain of device-to-device copies into the successor's buffer
  * through CUDA IPC mappings -- executed by the copy engines, so the GEMM keeps
- * every SM (tm_sgemm_dist leaves 16 to NCCL's kernels).  Each 256-K-row piece
+ * every SM (tm_sgemm_dist leaves 16 to NCCL's kernels).  Each 128-K-row piece
  * is flagged on arrival with a stream memory operation; a rank gives its
  * predecessor a credit (its B is free) at the start of every call.
  *

@@ -366,18 +366,22 @@ def dist_chunks(k: int, nranks: int):
 
 
 def sgemm_dist_loopback(m, n, k, A_locals, Bs, C_locals, alpha=1.0, beta=0.0, root=0, stream=None, allgather=False,
-                        fused=False):
+                        fused=False, transport="nccl"):
     """Single-process emulation of the row-sharded mode:
     len(A_locals) simulated ranks on the current GPU, same schedule as
     Comm.sgemm (or Comm.sgemm_allgather when allgather=True: Bs[r] holds rank
     r's k-row shard in place; or Comm.sgemm(fused=True)'s flag-gated single
-    launch when fused=True).  Returns the bytes each simulated rank received."""
+    launch when fused=True).  transport="ce": the copy-engine transport MODEL
+    (tm.h modes 3, 4: no data moves -- fill every Bs[r] with B first -- chunks
+    are released on a link-rate schedule, GEMMs keep every SM but one).
+    Returns the bytes each simulated rank received."""
     P = len(A_locals)
     arr = lambda ts: (ctypes.c_void_p * P)(*[t.data_ptr() for t in ts])
     lda = next((_ld(a) for a in A_locals if a.shape[0] > 0), max(k, 1))
     ldc = next((_ld(c) for c in C_locals if c.shape[0] > 0), max(n, 1))
     got = (ctypes.c_uint64 * P)()
-    st = lib.tm_sgemm_dist_loopback(P, int(root), 1 if allgather else 2 if fused else 0, m, n, k, float(alpha), arr(A_locals), lda,
+    mode = 1 if allgather else (2 if fused else 0) + (2 if transport == "ce" else 0)
+    st = lib.tm_sgemm_dist_loopback(P, int(root), mode, m, n, k, float(alpha), arr(A_locals), lda,
                                     arr(Bs), _ld(Bs[0]),
                                     float(beta), arr(C_locals), ldc, got, _stream(stream))
     _check(st, "tm_sgemm_dist_loopback")

@@ -164,6 +164,8 @@ tm_status run(const GemmArgs& a, int algo, cudaStream_t stream, int sm_reserve =
   if (st != TM_OK) return st;
   // sm_reserve: SMs left free for concurrent kernels (the distributed mode's
   // NCCL broadcast must be able to run beside the persistent GEMM).
+  if (sm_reserve == 0)
+    if (const char* e = std::getenv("TM_SM_RESERVE")) sm_reserve = std::atoi(e);  // projection knob (scripts/)
   const int sms = (sm_reserve > 0 && dev->sms - sm_reserve >= 2) ? dev->sms - sm_reserve : dev->sms;
   Plan pl = make_plan(a, algo, sms);
   // NVTX range around the enqueue (visible in Nsight Systems; no-op without a tool)

@@ -6,12 +6,15 @@
 // Here the one exchange, B from the root to every rank, runs as a pipelined
 // chain root -> r+1 -> r+2 ... over CUDA IPC mappings of the peers' buffers:
 // each rank PUSHES every piece of B it holds into its successor's B with a
-// device-to-device cudaMemcpyAsync (executed by the copy engines: measured,
-// scripts/r02/ce_probe.cu, a 256 MiB copy completes while a kernel holds
-// every SM), then writes the successor's arrival flag for that piece with a
-// stream memory operation (cuStreamWriteValue32, ordered after the copy, with
-// a memory barrier).  No kernel moves data, so the GEMM keeps all 148 SMs
-// (the NCCL schedule leaves 16 to NCCL's kernels).
+// cudaMemcpyAsync to the peer's mapping -- between devices a peer-to-peer copy
+// over NVLink, executed by the copy engines -- then writes the successor's
+// arrival flag for that piece with a stream memory operation
+// (cuStreamWriteValue32, ordered after the copy, with a memory barrier).  No
+// kernel moves data between GPUs, so the GEMM keeps all 148 SMs (the NCCL
+// schedule leaves 16 to NCCL's kernels).  Within ONE device a device-to-device
+// cudaMemcpyAsync is a kernel (scripts/r02/ce_probe.cu: a 256 MiB copy waits
+// 3 ms behind a kernel holding every SM's thread slots), so the tests, whose
+// processes share one GPU, check correctness only, not overlap.
 //
 // Flow control (credits): before the first piece of a call is pushed, the
 // successor must have declared its B free for this call: every rank writes
@@ -39,7 +42,7 @@ namespace {
 
 constexpr int kMaxPieces = 4096;
 constexpr int kMaxChunksCe = 16;
-constexpr int64_t kPieceRows = 256;  // K-rows per forwarded piece (16 MiB at n = 16384)
+constexpr int64_t kPieceRows = 128;  // K-rows per forwarded piece (8 MiB at n = 16384)
 
 }  // namespace
 

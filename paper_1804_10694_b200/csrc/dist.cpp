@@ -27,6 +27,9 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <chrono>
+#include <thread>
+#include <vector>
 
 #include "tm_internal.h"
 
@@ -116,32 +119,45 @@ constexpr int kMaxChunks = 16;
 
 tm_status set_flag(cudaStream_t s, unsigned* flag, unsigned value) { return tmk::stream_write_u32(s, flag, value); }
 
-// Loopback link model (projection only, TM_LOOPBACK_LINK_GBS): after each
-// chunk's on-device copy the transfer stream spins for bytes / rate, so the
-// chunk "arrives" no earlier than a link of that rate would deliver it (the
-// copy's own time comes on top: a conservative model).
-__global__ void k_link_delay(unsigned long long ns) {
-  unsigned long long t0, t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  do {
-    __nanosleep(500);
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  } while (t - t0 < ns);
+// Loopback link model (projections, TM_LOOPBACK_LINK_GBS = R GB/s): a
+// rank's transfer stream starts a clock before its first chunk and, after
+// chunk c (its device copy in modes 0-2), blocks until
+//   t0 + (chain_pos * piece_bytes + bytes of chunks 0..c) / R,
+// so chunk c arrives no earlier than a pipelined chain (or ring) of links of
+// rate R delivers it to the rank at position chain_pos.  The clock and the
+// waits are host functions on the transfer stream (cudaLaunchHostFunc): they
+// hold the stream without occupying an SM, so the GEMMs keep theirs.
+struct LinkClock {
+  std::chrono::steady_clock::time_point t0;
+};
+struct LinkWait {
+  LinkClock* clock;
+  double ns;
+};
+void CUDART_CB link_start(void* p) { static_cast<LinkClock*>(p)->t0 = std::chrono::steady_clock::now(); }
+void CUDART_CB link_until(void* p) {
+  const LinkWait* w = static_cast<const LinkWait*>(p);
+  std::this_thread::sleep_until(w->clock->t0 + std::chrono::nanoseconds(static_cast<long long>(w->ns)));
 }
-// SMs the loopback's fused GEMM leaves free for its transfers: a same-device
-// cudaMemcpyAsync runs on SMs (measured: with 2 free SMs the 1 GiB broadcast
-// took ~10 ms), so the loopback reserves as many as the NCCL mode does
-// (TM_LOOPBACK_RESERVE overrides; the link-model delay kernel needs one).
-int loopback_reserve() {
+// SMs the loopback's GEMMs leave free.  NCCL model (modes 0-2): as many as
+// the NCCL schedule leaves to NCCL's kernels -- the loopback's same-device
+// copies are kernels too (scripts/r02/ce_probe.cu: a 256 MiB device-to-device
+// copy waits 3 ms behind a kernel that holds every SM's thread slots).
+// Copy-engine model (modes 3, 4): none; the chunks are not copied at all
+// (peer-to-peer copies between devices run on the copy engines, which one
+// device cannot emulate), only released on the link model's schedule.
+int loopback_reserve(int mode) {
+  if (mode >= 3) return 0;
   static const int v = [] {
     const char* e = std::getenv("TM_LOOPBACK_RESERVE");
     return e ? std::max(1, std::atoi(e)) : comm_ctas();
   }();
   return v;
 }
-double loopback_link_gbs() {
+double loopback_link_gbs(int mode) {
   const char* e = std::getenv("TM_LOOPBACK_LINK_GBS");
-  return e ? std::atof(e) : 0.0;
+  const double v = e ? std::atof(e) : 0.0;
+  return mode >= 3 && v <= 0.0 ? 700.0 : v;
 }
 
 }  // namespace
@@ -416,7 +432,7 @@ template <class Xfer>
 tm_status dist_schedule(int nranks, int rank, int root, int64_t m, int64_t n, int64_t k, float alpha,
                         const float* A_local, int64_t lda, float* B, int64_t ldb, float beta, float* C_local,
                         int64_t ldc, cudaStream_t stream, cudaStream_t comm_stream, cudaEvent_t ev_start,
-                        cudaEvent_t* ev_chunk, uint64_t* bytes_received, Xfer&& xfer) {
+                        cudaEvent_t* ev_chunk, uint64_t* bytes_received, Xfer&& xfer, int reserve_sms = -1) {
   int64_t row0 = 0, rows = 0;
   tm_dist_rows(m, nranks, rank, &row0, &rows);
   const bool reads_ab = alpha != 0.0f && k > 0 && n > 0;
@@ -447,7 +463,8 @@ tm_status dist_schedule(int nranks, int rank, int root, int64_t m, int64_t n, in
     if (cudaStreamWaitEvent(stream, ev_chunk[c], 0) != cudaSuccess) return TM_ERR_CUDA;
     if (rows > 0) {
       tmk::GemmArgs ga{rows, n, kr, alpha, c == 0 ? beta : 1.0f, A_local + k0, lda, B + k0 * ldb, ldb, C_local, ldc};
-      const int reserve = chunk_overlaps_transfer(bounds, c, nchunks, rows, n, ldb) ? comm_ctas() : 0;
+      const int reserve = reserve_sms >= 0 ? reserve_sms
+                          : chunk_overlaps_transfer(bounds, c, nchunks, rows, n, ldb) ? comm_ctas() : 0;
       tm_status st = tmk::sgemm_reserve(ga, stream, reserve);
       if (st != TM_OK) return st;
     }
@@ -481,7 +498,7 @@ tm_status dist_fused_schedule(int nranks, int rank, int root, int64_t m, int64_t
   tmk::GemmArgs ga{rows, n, k, alpha, beta, A_local, lda, B, ldb, C_local, ldc};
   if (rows > 0 && !tmk::tc_plan_ok(ga))
     return dist_schedule(nranks, rank, root, m, n, k, alpha, A_local, lda, B, ldb, beta, C_local, ldc, stream,
-                         comm_stream, ev_start, ev_chunk, bytes_received, xfer);
+                         comm_stream, ev_start, ev_chunk, bytes_received, xfer, reserve == comm_ctas() ? -1 : reserve);
   int64_t bounds[kMaxChunks + 1];
   const int nchunks = uniform_plan(k, nranks, bounds);  // flags cover equal chunks of kc rows
   const int64_t kc = bounds[1];
@@ -643,7 +660,7 @@ tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int6
                                  float beta, float* const* C_locals, int64_t ldc, uint64_t* bytes_received,
                                  void* stream_) {
   if (nranks < 1 || root < 0 || root >= nranks || !A_locals || !Bs || !C_locals || m < 0 || n < 0 || k < 0 ||
-      mode < 0 || mode > 2)
+      mode < 0 || mode > 4)
     return TM_ERR_INVALID_VALUE;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   cudaStream_t cs = nullptr;
@@ -654,11 +671,14 @@ tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int6
   for (int i = 0; ok && i < kMaxChunks; ++i)
     ok = cudaEventCreateWithFlags(&ev_chunk[i], cudaEventDisableTiming) == cudaSuccess;
   unsigned* flags = nullptr;  // fused mode: per-chunk arrival flags, zeroed once (rank r's epoch is r + 1)
-  if (ok && mode == 2)
+  LinkClock clock;                 // link model (host functions on the transfer stream)
+  std::vector<LinkWait> waits;
+  waits.reserve(kMaxChunks);
+  if (ok && (mode == 2 || mode == 4))
     ok = cudaMalloc(&flags, kMaxChunks * sizeof(unsigned)) == cudaSuccess &&
          cudaMemsetAsync(flags, 0, kMaxChunks * sizeof(unsigned), stream) == cudaSuccess;
   if (!ok) st = TM_ERR_CUDA;
-  const double link_gbs = loopback_link_gbs();
+  const double link_gbs = loopback_link_gbs(mode);
   if (bytes_received)
     for (int r = 0; r < nranks; ++r) bytes_received[r] = 0;
   // Ranks run one after another on this device; rank r's "broadcast" copies
@@ -677,25 +697,36 @@ tm_status tm_sgemm_dist_loopback(int nranks, int root, int mode, int64_t m, int6
     if (st == TM_OK && cudaStreamSynchronize(stream) != cudaSuccess) st = TM_ERR_CUDA;
   }
   for (int r = 0; st == TM_OK && r < nranks; ++r) {
-    if (mode == 0 || mode == 2) {
+    if (mode != 1) {
       const float* root_B = Bs[root];
+      const int pos = (r - root + nranks) % nranks;                       // chain position
+      const double piece_bytes = 128.0 * static_cast<double>(ldb) * 4.0;  // the CE chain's piece
+      double sent = 0.0;
       auto xfer = [&](float* p, size_t count) -> tm_status {
         if (r == root) return TM_OK;
+        if (link_gbs > 0.0 && p == Bs[r]) {  // first chunk: start the link clock
+          waits.clear();
+          if (cudaLaunchHostFunc(cs, link_start, &clock) != cudaSuccess) return TM_ERR_CUDA;
+        }
         const float* src = root_B + (p - Bs[r]);
-        if (cudaMemcpyAsync(p, src, count * 4, cudaMemcpyDeviceToDevice, cs) != cudaSuccess) return TM_ERR_CUDA;
-        if (link_gbs > 0.0) {  // projection: the chunk arrives at the modelled link rate
-          k_link_delay<<<1, 1, 0, cs>>>(static_cast<unsigned long long>(count * 4.0 / link_gbs));
-          if (cudaGetLastError() != cudaSuccess) return TM_ERR_CUDA;
+        if (mode < 3 && cudaMemcpyAsync(p, src, count * 4, cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
+          return TM_ERR_CUDA;
+        if (link_gbs > 0.0) {  // projection: the chunk arrives no earlier than the modelled link delivers it
+          sent += count * 4.0;
+          waits.push_back({&clock, (pos * piece_bytes + sent) / link_gbs});
+          if (cudaLaunchHostFunc(cs, link_until, &waits.back()) != cudaSuccess) return TM_ERR_CUDA;
         }
         return TM_OK;
       };
-      if (mode == 0)
+      const int reserve = loopback_reserve(mode);
+      if (mode == 0 || mode == 3)
         st = dist_schedule(nranks, r, root, m, n, k, alpha, A_locals[r], lda, Bs[r], ldb, beta, C_locals[r], ldc,
-                           stream, cs, ev_start, ev_chunk, bytes_received ? &bytes_received[r] : nullptr, xfer);
+                           stream, cs, ev_start, ev_chunk, bytes_received ? &bytes_received[r] : nullptr, xfer,
+                           mode == 3 ? reserve : -1);
       else  // flags of simulated rank r carry epoch r + 1 (flags are never reset within the call)
         st = dist_fused_schedule(nranks, r, root, m, n, k, alpha, A_locals[r], lda, Bs[r], ldb, beta, C_locals[r],
                                  ldc, stream, cs, ev_start, ev_chunk, flags, static_cast<unsigned>(r + 1),
-                                 loopback_reserve(), bytes_received ? &bytes_received[r] : nullptr, xfer);
+                                 reserve, bytes_received ? &bytes_received[r] : nullptr, xfer);
     } else {
       auto gather = [&](size_t count) -> tm_status {
         for (int q = 0; q < nranks; ++q) {

@@ -20,7 +20,13 @@ namespace tmk {
 
 // Stream-K pays off when the data-parallel schedule leaves a partial last
 // wave that matters: fewer than 8 waves, tiles not a multiple of the cluster
-// count, and at least 2 K-blocks of work per cluster.
+// count, and at least 2 K-blocks of work per cluster.  Except for long-K
+// schedules of >= 2 waves whose last wave is nearly full: data-parallel, they
+// keep the clusters in step with the wave barrier (tc_gemm.cuh; L2 panel
+// reuse), which stream-K cannot, and under the sustained power cap that is
+// worth more than the partial wave: one rank of the 8-way row-sharded C5,
+// 2048 x 16384 x 16384 = 512 tiles on 74 clusters (6.92 waves), runs in
+// 4.01 ms data-parallel vs 4.70 ms stream-K (scripts/r02/rank_probe.py).
 bool plan_streamk(int64_t m, int64_t n, int64_t k, int cg, int bn_cta, int num_sms) {
   const int64_t tile_m = 128LL * cg, tile_n = static_cast<int64_t>(bn_cta) * cg;
   const int64_t tiles = ((m + tile_m - 1) / tile_m) * ((n + tile_n - 1) / tile_n);
@@ -28,6 +34,9 @@ bool plan_streamk(int64_t m, int64_t n, int64_t k, int cg, int bn_cta, int num_s
   const int64_t kb = (k + 31) / 32;
   if (tiles % units == 0) return false;
   if (tiles >= 8 * units) return false;
+  const int64_t waves = (tiles + units - 1) / units;
+  const double wave_fill = static_cast<double>(tiles) / static_cast<double>(waves * units);
+  if (kb >= 64 && tiles >= 2 * units && wave_fill >= 0.9) return false;
   return tiles * kb >= 2 * units;
 }
 

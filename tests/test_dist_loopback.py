@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-def _run(P, root, m, n, k, seed, kind="uniform", ldb=None, fused=False):
+def _run(P, root, m, n, k, seed, kind="uniform", ldb=None, fused=False, transport="nccl"):
     import torch
     import paper_1804_10694_b200 as tm
     ldb = n if ldb is None else ldb
@@ -30,22 +30,26 @@ def _run(P, root, m, n, k, seed, kind="uniform", ldb=None, fused=False):
         parts.append((r0, rows))
         As.append(dA[r0:r0 + rows])
         Cs.append(torch.from_numpy(np.ascontiguousarray(C0[r0:r0 + rows])).cuda())
-        if r == root:
+        if r == root or transport == "ce":  # the copy-engine model moves no data (tm.h)
             Bs.append(torch.from_numpy(Bfull).cuda())
         else:
             Bs.append(torch.full((k, ldb), float("nan"), dtype=torch.float32, device="cuda"))
-    got = tm.sgemm_dist_loopback(m, n, k, As, [b for b in Bs], Cs, si.ALPHA, si.BETA, root=root, fused=fused)
+    got = tm.sgemm_dist_loopback(m, n, k, As, [b for b in Bs], Cs, si.ALPHA, si.BETA, root=root, fused=fused,
+                                 transport=transport)
     torch.cuda.synchronize()
     return A, B, C0, parts, [c.cpu().numpy() for c in Cs], got, [b[:, :n].cpu().numpy() for b in Bs]
 
 
+@pytest.mark.parametrize("transport", ["nccl", "ce"])
 @pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("P,root", [(2, 0), (3, 1), (8, 0), (8, 5)])
-def test_loopback_shards_match_oracle(P, root, fused):
+def test_loopback_shards_match_oracle(P, root, fused, transport):
     """fused=False: K-chunked schedule (beta chain); fused=True: one GEMM per
-    rank whose TMA producers wait on per-chunk flags set by the copy stream."""
+    rank whose TMA producers wait on per-chunk flags set by the copy stream.
+    transport="ce": the copy-engine transport model (every B pre-filled, chunks
+    released on the link model's schedule, GEMMs on every SM but one)."""
     m, n, k = 1060, 260, 1100   # uneven rows; two K-chunks of 512 and 588
-    A, B, C0, parts, Cs, got, Bs = _run(P, root, m, n, k, seed=40 + P, fused=fused)
+    A, B, C0, parts, Cs, got, Bs = _run(P, root, m, n, k, seed=40 + P, fused=fused, transport=transport)
     R, D = oracle.sgemm(si.ALPHA, A, B, si.BETA, C0)
     for r, ((r0, rows), C) in enumerate(zip(parts, Cs)):
         assert C.shape == (rows, n)
