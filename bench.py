@@ -158,6 +158,33 @@ class ClockSampler:
         return out
 
 
+# Test-only: TM_BENCH_SHARED_GPU=1 puts every rank on cuda:0 with a gloo
+# process group, so the N > 1 code path (barriers, max over ranks, the
+# copy-engine transport) can be exercised on a one-GPU box.  Its timings are
+# meaningless (the ranks time-slice one GPU) and say so in the JSON line.
+SHARED_GPU = os.environ.get("TM_BENCH_SHARED_GPU") == "1"
+
+
+def init_dist(torch, dist, world, local):
+    """Binds this rank's GPU and, for N > 1, the process group; returns the GPU index."""
+    dev = 0 if SHARED_GPU else local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if SHARED_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    return dev
+
+
+def max_over_ranks(torch, dist, world, values):
+    """Element-wise max over ranks of a list of floats (CUDA events' ms)."""
+    t = torch.tensor(values, dtype=torch.float64, device="cpu" if SHARED_GPU else "cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
 def workload(name):
     import seeded_inputs as si
     m, n, k = si.CONFIGS[name]
@@ -274,6 +301,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C3b", "C4", "C5", "CONV", "BLUR"])
     ap.add_argument("--algo", default="auto", choices=list(ALGOS))
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ce"],
+                    help="N > 1: B broadcast by NCCL (tm_sgemm_dist) or the copy-engine chain (tm_sgemm_dist_ce)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--conv-beta", type=float, default=0.0)
@@ -298,9 +327,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = init_dist(torch, dist, world, local)
     peaks = load_peaks()
     m, n, k, desc = workload(args.config)
     alpha, beta = si.ALPHA, si.BETA
@@ -314,7 +341,8 @@ def main():
     else:
         r0, rows = tm.dist_rows(m, world, rank)
         A, B, C = make_inputs(args.config, m, n, k, (r0, rows))
-    comm = tm.Comm(rank, world) if world > 1 else None
+    comm = (tm.CeComm(rank, world) if args.transport == "ce" else tm.Comm(rank, world)) if world > 1 else None
+    ce_handles = comm.exchange(B) if args.transport == "ce" and comm is not None else None
     in_bytes = 4 * (m * k + k * n + m * n)
     small = in_bytes < 2 * 126 * 2 ** 20  # inputs fit in L2: flush between iterations
     # L2 flush by READING 512 MiB (a write-flush would leave ~126 MB of dirty
@@ -326,7 +354,10 @@ def main():
         if comm is None:
             tm.sgemm_ex(A, B, C, alpha, beta, algo)
         else:
-            comm.sgemm(m, n, k, A, B, C, alpha, beta, root=0)
+            if ce_handles is not None:
+                comm.sgemm(m, n, k, A, B, C, alpha, beta, root=0, handles=ce_handles)
+            else:
+                comm.sgemm(m, n, k, A, B, C, alpha, beta, root=0)
 
     path = tm.plan_name(rows, n, k, alpha, beta, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
                         C.data_ptr(), C.stride(0), algo)
@@ -368,10 +399,7 @@ def main():
     per_step = [a.elapsed_time(b) for a, b in ev]  # ms, device time of each step's hot path
     total_ms = sum(per_step)
     med_ms = statistics.median(per_step)
-    t = torch.tensor([total_ms, med_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, med_ms = float(t[0].item()), float(t[1].item())
+    total_ms, med_ms = max_over_ranks(torch, dist, world, [total_ms, med_ms])
     ms_per_step = total_ms / args.steps
     flops = 2.0 * m * n * k
     value = flops * args.steps / (total_ms * 1e-3) / 1e9  # GFLOP/s, whole job
@@ -421,9 +449,12 @@ def main():
             kernel, "f32 (3xTF32 tensor-core, fp32 accumulate)"), "data": "synthetic (seeded U[-1,1) fp32, device-generated)",
         "config": {"workload": desc, "m": m, "n": n, "k": k, "alpha": alpha, "beta": beta, "path": path,
                    "rows_per_rank": rows, "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                   "transport": (args.transport if world > 1 else None),
                    "l2": "inputs larger than L2, no flush" if not small else "L2 flushed (512 MiB read) between steps"},
         "roofline": roof, "gpu_launches": launches, "clocks": clocks.summary(),
     }
+    if SHARED_GPU and world > 1:
+        line["note"] = "TM_BENCH_SHARED_GPU: all ranks time-slice cuda:0 -- a code-path check, not a measurement"
 
     # e2e through the public API with host buffers (copies inside the timed region)
     if not args.no_e2e:
@@ -523,9 +554,7 @@ def run_blur(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = init_dist(torch, dist, world, local)
     N, M = si.BLUR_IMAGE
     img = si.image(N, M)
     r0, rows = tm.dist_rows(N - 2, world, rank)
@@ -533,7 +562,8 @@ def run_blur(args):
     if world > 1 and rank < world - 1:
         lin[rows:] = float("nan")  # received from rank + 1 every step
     lout = torch.empty((rows, M - 2, 3), dtype=torch.float32, device="cuda")
-    comm = tm.Comm(rank, world) if world > 1 else None
+    comm = (tm.CeComm(rank, world) if args.transport == "ce" else tm.Comm(rank, world)) if world > 1 else None
+    ce_handles = comm.exchange(B) if args.transport == "ce" and comm is not None else None
     flush = torch.ones(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
     flush_out = torch.empty(1, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
@@ -570,10 +600,7 @@ def run_blur(args):
             dist.barrier()
         clocks.mark_region(t0_host, time.time())
     per_step = [a.elapsed_time(b) for a, b in ev]
-    t = torch.tensor([sum(per_step), statistics.median(per_step)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, med_ms = float(t[0].item()), float(t[1].item())
+    total_ms, med_ms = max_over_ranks(torch, dist, world, [sum(per_step), statistics.median(per_step)])
     algo_bytes = 12 * (N * M + (N - 2) * (M - 2))
     value = algo_bytes * args.steps / (total_ms * 1e-3) / 1e9
     my_bytes = 12 * ((rows + 2) * M + rows * (M - 2))
@@ -651,10 +678,7 @@ def measure_e2e(tm, torch, dist, world, rank, m, n, k, rows, alpha, beta, algo, 
         step()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dt = float(t.item())
+    dt = max_over_ranks(torch, dist, world, [dt])[0]
     return {"value": round(2.0 * m * n * k * steps / dt / 1e9, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 4 * rows * n, "steps": steps,
             "note": "tm_sgemm_host: pinned host A,B,C -> device, GEMM, C -> host, per step (host wall clock, synchronised)"
