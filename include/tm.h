@@ -341,6 +341,49 @@ tm_status tm_sgemm_dist_allgather(tm_comm_t comm, int64_t m, int64_t n, int64_t 
                                   int64_t ldc, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * 2-D SUMMA sharding ("2-D SUMMA-style sharding for
+ * larger P"; the paper's distribute / send / receive, PAPER.md:311,
+ * PAPER.md:323-335, generalised from rows to a grid).
+ *
+ * nranks = pr * pc; rank r is grid position (i, j) = (r / pc, r % pc) and owns
+ *   C_local = C[rows_i, cols_j]   (rows_i x cols_j, ldc)
+ *   A_local = A[rows_i, ka_j]     (rows_i x |ka_j|, lda >= |ka_j|)
+ *   B_local = B[kb_i, cols_j]     (|kb_i| x cols_j, ldb >= cols_j)
+ * with rows_i = tm_dist_rows(m, pr, i), cols_j = tm_dist_rows(n, pc, j),
+ * ka_j = tm_dist_rows(k, pc, j), kb_i = tm_dist_rows(k, pr, i).  K is cut into
+ * panels (tm_summa_panel) each inside one A column block and one B row block;
+ * per panel the owner of A(i, panel) broadcasts it along grid row i and the
+ * owner of B(panel, j) along grid column j (NCCL, row / column communicators
+ * split from the communicator on the first call with a grid), and every rank
+ * accumulates C_local = alpha * A(i, panel) B(panel, j) + beta_p C_local (beta
+ * for the first panel, then 1).  Panels are double-buffered in library memory
+ * owned by the communicator.  On return (stream-ordered) C_local = alpha *
+ * A[rows_i, :] B[:, cols_j] + beta C_local; inputs are not modified.
+ * Collective: all ranks call with the same pr, pc, m, n, k, alpha, beta.
+ * Errors: pr * pc != nranks or bad sizes -> TM_ERR_INVALID_VALUE; NCCL
+ * failure -> TM_ERR_NCCL; panel buffers -> TM_ERR_OUT_OF_MEMORY. */
+tm_status tm_sgemm_summa(tm_comm_t comm, int pr, int pc, int64_t m, int64_t n, int64_t k, float alpha,
+                         const float* A_local, int64_t lda, const float* B_local, int64_t ldb, float beta,
+                         float* C_local, int64_t ldc, void* stream);
+
+/* Panel plan of tm_sgemm_summa (host-only): idx < 0 returns the panel count in
+ * *k0; otherwise panel idx's K range [*k0, *k0 + *kr).  Panels tile [0, k) in
+ * order, each inside one block of tm_dist_rows(k, pc, .) and of
+ * tm_dist_rows(k, pr, .), at most 2048 long. */
+tm_status tm_summa_panel(int64_t k, int pr, int pc, int idx, int64_t* k0, int64_t* kr);
+
+/* Single-process loopback of tm_sgemm_summa (verification): pr * pc simulated
+ * ranks on the current device one after another; every panel is packed
+ * straight from its owner's block (device copies) instead of broadcast.
+ * Arrays of nranks entries: A_locals / ldas, B_locals / ldbs, C_locals / ldcs
+ * as rank r's arguments; bytes_received: optional per-rank counters of panel
+ * bytes that came from another rank.  Synchronises `stream`. */
+tm_status tm_sgemm_summa_loopback(int pr, int pc, int64_t m, int64_t n, int64_t k, float alpha,
+                                  const float* const* A_locals, const int64_t* ldas, const float* const* B_locals,
+                                  const int64_t* ldbs, float beta, float* const* C_locals, const int64_t* ldcs,
+                                  uint64_t* bytes_received, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Copy-engine chain broadcast (the paper's explicit
  * send/receive between row-owning ranks).
  *

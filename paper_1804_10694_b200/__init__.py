@@ -31,6 +31,7 @@ EXPORTED_SYMBOLS = [
     "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_fused", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
     "tm_sgemm_tune", "tm_tune_cache_size", "tm_tune_cache_clear", "tm_tune_cache_save", "tm_tune_cache_load",
     "tm_sgemm_plan_config", "tm_blur", "tm_blur_dist", "tm_blur_dist_loopback",
+    "tm_sgemm_summa", "tm_summa_panel", "tm_sgemm_summa_loopback",
     "tm_ipc_export", "tm_ce_create", "tm_ce_connect", "tm_ce_destroy", "tm_ce_bytes_received", "tm_sgemm_dist_ce",
 ]
 
@@ -81,6 +82,9 @@ def _load():
     L.tm_blur.argtypes = [i64, i64, vp, i64, vp, i64, vp]
     L.tm_blur_dist.argtypes = [vp, i64, i64, vp, i64, vp, i64, vp]
     L.tm_blur_dist_loopback.argtypes = [ci, i64, i64, vp, i64, vp, i64, vp, vp]
+    L.tm_sgemm_summa.argtypes = [vp, ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp]
+    L.tm_summa_panel.argtypes = [i64, ci, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.tm_sgemm_summa_loopback.argtypes = [ci, ci, i64, i64, i64, f32, vp, vp, vp, vp, f32, vp, vp, vp, vp]
     L.tm_ipc_export.argtypes = [vp, vp]
     L.tm_ce_create.argtypes = [ctypes.POINTER(vp), ci, ci, vp]
     L.tm_ce_connect.argtypes = [vp, vp]
@@ -388,6 +392,38 @@ def sgemm_dist_loopback(m, n, k, A_locals, Bs, C_locals, alpha=1.0, beta=0.0, ro
     return [int(x) for x in got]
 
 
+def summa_panels(k: int, pr: int, pc: int):
+    """Panel plan of the 2-D SUMMA schedule: list of (k0, kr)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.tm_summa_panel(k, pr, pc, -1, ctypes.byref(a), ctypes.byref(b)), "tm_summa_panel")
+    out = []
+    for i in range(a.value):
+        _check(lib.tm_summa_panel(k, pr, pc, i, ctypes.byref(a), ctypes.byref(b)), "tm_summa_panel")
+        out.append((a.value, b.value))
+    return out
+
+
+def summa_blocks(m, n, k, pr, pc, rank):
+    """(rows_i, cols_j, ka_j, kb_i) of grid rank r = (r // pc, r % pc): each a
+    (start, length) pair -- the blocks of C, A and B it owns (tm.h SUMMA)."""
+    i, j = rank // pc, rank % pc
+    return dist_rows(m, pr, i), dist_rows(n, pc, j), dist_rows(k, pc, j), dist_rows(k, pr, i)
+
+
+def sgemm_summa_loopback(pr, pc, m, n, k, A_locals, B_locals, C_locals, alpha=1.0, beta=0.0, stream=None):
+    """Single-process emulation of Comm.sgemm_summa over a pr x pc grid on the
+    current GPU; A_locals[r], B_locals[r], C_locals[r] are rank r's blocks
+    (summa_blocks).  Returns the panel bytes each simulated rank received."""
+    P = pr * pc
+    ptrs = lambda ts: (ctypes.c_void_p * P)(*[t.data_ptr() for t in ts])
+    lds = lambda ts: (ctypes.c_int64 * P)(*[_ld(t) if t.shape[0] > 0 and t.shape[1] > 0 else max(1, t.shape[1]) for t in ts])
+    got = (ctypes.c_uint64 * P)()
+    st = lib.tm_sgemm_summa_loopback(pr, pc, m, n, k, float(alpha), ptrs(A_locals), lds(A_locals), ptrs(B_locals),
+                                     lds(B_locals), float(beta), ptrs(C_locals), lds(C_locals), got, _stream(stream))
+    _check(st, "tm_sgemm_summa_loopback")
+    return [int(x) for x in got]
+
+
 def _image(name, t, rows=None, cols=None):
     """(pointer, row pitch in floats) of an (N, M, 3) float32 CUDA image whose
     rows may be padded (strides (ld, 3, 1))."""
@@ -600,3 +636,13 @@ class Comm:
         po, ldo = _image("lout", lout, rows, M - 2)
         _check(lib.tm_blur_dist(self.handle, N, M, pi, ldi, po, ldo, _stream(stream)), "tm_blur_dist")
         return lout
+
+    def sgemm_summa(self, pr, pc, m, n, k, A_local, B_local, C_local, alpha=1.0, beta=0.0, stream=None):
+        """2-D SUMMA over a pr x pc grid (tm_sgemm_summa): this rank's blocks
+        (summa_blocks(m, n, k, pr, pc, rank)); C_local updated in place."""
+        ld = lambda t, w: _ld(t) if t is not None and t.shape[0] > 0 and t.shape[1] > 0 else max(1, w)
+        st = lib.tm_sgemm_summa(self.handle, int(pr), int(pc), m, n, k, float(alpha), _ptr(A_local),
+                                ld(A_local, A_local.shape[1]), _ptr(B_local), ld(B_local, B_local.shape[1]),
+                                float(beta), _ptr(C_local), ld(C_local, C_local.shape[1]), _stream(stream))
+        _check(st, "tm_sgemm_summa")
+        return C_local

@@ -78,6 +78,7 @@ struct Nccl {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, NcclConfig*) = nullptr;
   bool ok = false;
 };
 
@@ -107,6 +108,7 @@ void load_nccl() {
   g_nccl.Recv = reinterpret_cast<decltype(g_nccl.Recv)>(dlsym(h, "ncclRecv"));
   g_nccl.GroupStart = reinterpret_cast<decltype(g_nccl.GroupStart)>(dlsym(h, "ncclGroupStart"));
   g_nccl.GroupEnd = reinterpret_cast<decltype(g_nccl.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+  g_nccl.CommSplit = reinterpret_cast<decltype(g_nccl.CommSplit)>(dlsym(h, "ncclCommSplit"));
   g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.Broadcast && g_nccl.AllGather;
 }
 
@@ -222,6 +224,13 @@ struct tm_comm_s {
   uint64_t bytes_received = 0;
   unsigned* chunk_flags = nullptr;  // [kMaxChunks] device arrival flags (fused mode)
   unsigned epoch = 0;               // fused-mode call counter (the flag value of this call)
+  // SUMMA (tm_sgemm_summa): row / column communicators of the last grid,
+  // double-buffered panel buffers, their events
+  int summa_pr = 0, summa_pc = 0;
+  ncclComm_t row_comm = nullptr, col_comm = nullptr;
+  float* panel_buf = nullptr;
+  size_t panel_bytes = 0;
+  cudaEvent_t ev_ready[2] = {}, ev_used[2] = {};
 };
 
 extern "C" {
@@ -293,6 +302,13 @@ tm_status tm_comm_destroy(tm_comm_t c) {
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->chunk_flags) cudaFree(c->chunk_flags);
+  if (c->row_comm) g_nccl.CommDestroy(c->row_comm);
+  if (c->col_comm) g_nccl.CommDestroy(c->col_comm);
+  if (c->panel_buf) cudaFree(c->panel_buf);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_ready[i]) cudaEventDestroy(c->ev_ready[i]);
+    if (c->ev_used[i]) cudaEventDestroy(c->ev_used[i]);
+  }
   delete c;
   return st;
 }
@@ -574,6 +590,132 @@ tm_status allgather_schedule(int nranks, int rank, int64_t m, int64_t n, int64_t
   return TM_OK;
 }
 
+// ---------------------------------------------------------------- SUMMA
+// 2-D sharding ("2-D SUMMA-style sharding for larger
+// P"): ranks form a pr x pc grid, rank r = (i, j) = (r / pc, r % pc) owns
+//   C[rows_i, cols_j],  A[rows_i, ka_j],  B[kb_i, cols_j]
+// with rows_i = tm_dist_rows(m, pr, i), cols_j = tm_dist_rows(n, pc, j),
+// ka_j = tm_dist_rows(k, pc, j), kb_i = tm_dist_rows(k, pr, i).  K is cut into
+// panels lying inside one A column block and one B row block; for panel p the
+// owner (i, ja(p)) of A(i, p) broadcasts it along grid row i, the owner
+// (ib(p), j) of B(p, j) along grid column j, and every rank accumulates
+// C_ij = alpha * A(i,p) B(p,j) + beta_p C_ij (beta for the first panel, then
+// 1).  Double-buffered: panel p+1 is packed and broadcast while panel p's GEMM
+// runs.  Per rank the traffic is the A and B panels of its grid row / column
+// (~ k (m/pr + n/pc) floats) instead of all of B (k n) for the 1-D schedule.
+
+constexpr int64_t kSummaPanelMax = 2048;
+
+// Panel boundaries: the union of the A (over pc) and B (over pr) K
+// partitions, each interval split into pieces of at most kSummaPanelMax.
+static int summa_panels(int64_t k, int pr, int pc, std::vector<int64_t>& b) {
+  b.assign(1, 0);
+  if (k <= 0) return 0;
+  std::vector<int64_t> cuts;
+  for (int j = 0; j < pc; ++j) {
+    int64_t r0, rr;
+    tm_dist_rows(k, pc, j, &r0, &rr);
+    cuts.push_back(r0 + rr);
+  }
+  for (int i = 0; i < pr; ++i) {
+    int64_t r0, rr;
+    tm_dist_rows(k, pr, i, &r0, &rr);
+    cuts.push_back(r0 + rr);
+  }
+  std::sort(cuts.begin(), cuts.end());
+  int64_t prev = 0;
+  for (int64_t c : cuts) {
+    if (c <= prev) continue;
+    const int64_t pieces = (c - prev + kSummaPanelMax - 1) / kSummaPanelMax;
+    for (int64_t q = 1; q <= pieces; ++q) b.push_back(prev + (c - prev) * q / pieces);
+    prev = c;
+  }
+  return static_cast<int>(b.size()) - 1;
+}
+
+// The grid block owning K index k0 under tm_dist_rows(k, parts, .).
+static int owner_of(int64_t k, int parts, int64_t k0, int64_t* start) {
+  for (int q = 0; q < parts; ++q) {
+    int64_t r0, rr;
+    tm_dist_rows(k, parts, q, &r0, &rr);
+    if (k0 >= r0 && k0 < r0 + rr) {
+      *start = r0;
+      return q;
+    }
+  }
+  *start = 0;
+  return 0;
+}
+
+struct SummaBlocks {  // one rank's view: its blocks and those of the panel owners
+  int64_t rows, cols;                 // of C_ij
+  int64_t lda_panel, ldb_panel;       // packed panel pitches (multiples of 4)
+};
+
+// Per-rank SUMMA schedule.  `deliver(p, ja, ka0, ib, kb0, k0, kr, Apan, Bpan)`
+// enqueues on comm_stream the arrival of A(i, [k0, k0+kr)) packed as rows x kr
+// (pitch lda_panel) in Apan and B([k0, k0+kr), j) as kr x cols (pitch
+// ldb_panel) in Bpan; ja / ib own them, ka0 / kb0 are the owners' first K
+// indices.  panel_buf holds 2 x (A panel + B panel).
+template <class Deliver>
+tm_status summa_schedule(int pr, int pc, int rank, int64_t m, int64_t n, int64_t k, float alpha, float beta,
+                         float* C_local, int64_t ldc, cudaStream_t stream, cudaStream_t comm_stream,
+                         cudaEvent_t ev_start, cudaEvent_t* ev_ready, cudaEvent_t* ev_used, float* panel_buf,
+                         Deliver&& deliver) {
+  const int i = rank / pc, j = rank % pc;
+  int64_t r0, rows, c0, cols;
+  tm_dist_rows(m, pr, i, &r0, &rows);
+  tm_dist_rows(n, pc, j, &c0, &cols);
+  if (alpha == 0.0f || k == 0)  // every rank alike: nothing to exchange
+    return tm_sgemm(rows, cols, 0, 0.0f, nullptr, 1, nullptr, std::max<int64_t>(1, cols), beta, C_local, ldc, stream);
+  // A rank with an empty block still takes part in its row's and column's
+  // broadcasts (ranks of a grid row share `rows`, of a column `cols`).
+  std::vector<int64_t> b;
+  const int np = summa_panels(k, pr, pc, b);
+  int64_t maxkr = 0;
+  for (int p = 0; p < np; ++p) maxkr = std::max(maxkr, b[p + 1] - b[p]);
+  const int64_t lda_p = (maxkr + 3) / 4 * 4, ldb_p = (cols + 3) / 4 * 4;
+  const size_t a_elems = static_cast<size_t>(rows) * lda_p, b_elems = static_cast<size_t>(maxkr) * ldb_p;
+  if (cudaEventRecord(ev_start, stream) != cudaSuccess) return TM_ERR_CUDA;
+  if (cudaStreamWaitEvent(comm_stream, ev_start, 0) != cudaSuccess) return TM_ERR_CUDA;
+  nvtxRangePushA("tm_sgemm_summa schedule");
+  struct Pop {
+    ~Pop() { nvtxRangePop(); }
+  } pop;
+  for (int p = 0; p < np; ++p) {
+    const int s = p & 1;
+    float* Apan = panel_buf + s * (a_elems + b_elems);
+    float* Bpan = Apan + a_elems;
+    const int64_t k0 = b[p], kr = b[p + 1] - b[p];
+    int64_t ka0 = 0, kb0 = 0;
+    const int ja = owner_of(k, pc, k0, &ka0), ib = owner_of(k, pr, k0, &kb0);
+    if (p >= 2 && cudaStreamWaitEvent(comm_stream, ev_used[s], 0) != cudaSuccess) return TM_ERR_CUDA;
+    tm_status st = deliver(p, ja, ka0, ib, kb0, k0, kr, Apan, lda_p, Bpan, ldb_p);
+    if (st != TM_OK) return st;
+    if (cudaEventRecord(ev_ready[s], comm_stream) != cudaSuccess) return TM_ERR_CUDA;
+    if (cudaStreamWaitEvent(stream, ev_ready[s], 0) != cudaSuccess) return TM_ERR_CUDA;
+    if (rows > 0 && cols > 0) {
+      tmk::GemmArgs ga{rows, cols, kr, alpha, p == 0 ? beta : 1.0f, Apan, lda_p, Bpan, ldb_p, C_local, ldc};
+      if ((st = tmk::sgemm_reserve(ga, stream, 0)) != TM_OK) return st;
+    }
+    if (cudaEventRecord(ev_used[s], stream) != cudaSuccess) return TM_ERR_CUDA;
+  }
+  return TM_OK;
+}
+
+// Bytes of the two panel buffers (A and B, double-buffered) for rank `rank`.
+static size_t summa_buffer_bytes(int pr, int pc, int rank, int64_t m, int64_t n, int64_t k) {
+  int64_t r0, rows, c0, cols;
+  tm_dist_rows(m, pr, rank / pc, &r0, &rows);
+  tm_dist_rows(n, pc, rank % pc, &c0, &cols);
+  std::vector<int64_t> b;
+  const int np = summa_panels(k, pr, pc, b);
+  int64_t maxkr = 0;
+  for (int p = 0; p < np; ++p) maxkr = std::max(maxkr, b[p + 1] - b[p]);
+  const size_t a = static_cast<size_t>(rows) * ((maxkr + 3) / 4 * 4), bb = static_cast<size_t>(maxkr) * ((cols + 3) / 4 * 4);
+  return 2 * (a + bb) * 4;
+}
+
 // Row-distributed blur (Fig. 5 Code 3).  Rank r owns
 // output rows [row0, row0 + rows) of the N-2 (tm_dist_rows(N-2, P, r)) and the
 // matching input rows in lin[0, rows); the two border rows lin[rows, rows + 2)
@@ -812,6 +954,156 @@ tm_status tm_blur_dist_loopback(int nranks, int64_t N, int64_t M, float* const* 
   }
   if (cs) cudaStreamSynchronize(cs);
   if (ev_halo) cudaEventDestroy(ev_halo);
+  if (ev_start) cudaEventDestroy(ev_start);
+  if (cs) cudaStreamDestroy(cs);
+  return st;
+}
+
+tm_status tm_summa_panel(int64_t k, int pr, int pc, int idx, int64_t* k0, int64_t* kr) {
+  if (k < 0 || pr < 1 || pc < 1 || !k0 || !kr) return TM_ERR_INVALID_VALUE;
+  std::vector<int64_t> b;
+  const int np = summa_panels(k, pr, pc, b);
+  if (idx < 0) {
+    *k0 = np;
+    *kr = 0;
+    return TM_OK;
+  }
+  if (idx >= np) return TM_ERR_INVALID_VALUE;
+  *k0 = b[idx];
+  *kr = b[idx + 1] - b[idx];
+  return TM_OK;
+}
+
+tm_status tm_sgemm_summa(tm_comm_t comm, int pr, int pc, int64_t m, int64_t n, int64_t k, float alpha,
+                         const float* A_local, int64_t lda, const float* B_local, int64_t ldb, float beta,
+                         float* C_local, int64_t ldc, void* stream_) {
+  if (!comm || pr < 1 || pc < 1 || pr * pc != comm->nranks || m < 0 || n < 0 || k < 0) return TM_ERR_INVALID_VALUE;
+  const int r = comm->rank, i = r / pc, j = r % pc;
+  int64_t r0, rows, c0, cols, a0, ka, b0, kb;
+  tm_dist_rows(m, pr, i, &r0, &rows);
+  tm_dist_rows(n, pc, j, &c0, &cols);
+  tm_dist_rows(k, pc, j, &a0, &ka);
+  tm_dist_rows(k, pr, i, &b0, &kb);
+  if (rows > 0 && cols > 0 && (!C_local || ldc < std::max<int64_t>(1, cols))) return TM_ERR_INVALID_VALUE;
+  const bool reads_ab = alpha != 0.0f && k > 0;
+  if (reads_ab && ((ka > 0 && rows > 0 && (!A_local || lda < ka)) || (kb > 0 && cols > 0 && (!B_local || ldb < cols))))
+    return TM_ERR_INVALID_VALUE;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (comm->nranks == 1)
+    return tm_sgemm(m, n, k, alpha, A_local, lda, B_local, ldb, beta, C_local, ldc, stream);
+  if (!g_nccl.CommSplit || !g_nccl.GroupStart || !g_nccl.GroupEnd) return TM_ERR_NCCL;
+  if (comm->summa_pr != pr || comm->summa_pc != pc) {  // collective: every rank switches grid together
+    if (comm->row_comm) g_nccl.CommDestroy(comm->row_comm);
+    if (comm->col_comm) g_nccl.CommDestroy(comm->col_comm);
+    comm->row_comm = comm->col_comm = nullptr;
+    if (g_nccl.CommSplit(comm->comm, i, j, &comm->row_comm, nullptr) != ncclSuccess ||
+        g_nccl.CommSplit(comm->comm, j, i, &comm->col_comm, nullptr) != ncclSuccess)
+      return TM_ERR_NCCL;
+    comm->summa_pr = pr;
+    comm->summa_pc = pc;
+    for (int q = 0; q < 2; ++q) {
+      if (!comm->ev_ready[q] && cudaEventCreateWithFlags(&comm->ev_ready[q], cudaEventDisableTiming) != cudaSuccess)
+        return TM_ERR_CUDA;
+      if (!comm->ev_used[q] && cudaEventCreateWithFlags(&comm->ev_used[q], cudaEventDisableTiming) != cudaSuccess)
+        return TM_ERR_CUDA;
+    }
+  }
+  const size_t need = summa_buffer_bytes(pr, pc, r, m, n, k);
+  if (need > comm->panel_bytes) {
+    if (comm->panel_buf) {
+      cudaStreamSynchronize(comm->stream);
+      cudaStreamSynchronize(stream);
+      cudaFree(comm->panel_buf);
+      comm->panel_buf = nullptr;
+      comm->panel_bytes = 0;
+    }
+    if (cudaMalloc(&comm->panel_buf, need) != cudaSuccess) return TM_ERR_OUT_OF_MEMORY;
+    comm->panel_bytes = need;
+  }
+  auto deliver = [&](int, int ja, int64_t ka0, int ib, int64_t kb0, int64_t k0, int64_t kr, float* Apan,
+                     int64_t lda_p, float* Bpan, int64_t ldb_p) -> tm_status {
+    // owners pack their panel (a strided 2-D copy), then both broadcasts
+    if (j == ja && rows > 0 &&
+        cudaMemcpy2DAsync(Apan, lda_p * 4, A_local + (k0 - ka0), lda * 4, kr * 4, rows, cudaMemcpyDeviceToDevice,
+                          comm->stream) != cudaSuccess)
+      return TM_ERR_CUDA;
+    if (i == ib && cols > 0 &&
+        cudaMemcpy2DAsync(Bpan, ldb_p * 4, B_local + (k0 - kb0) * ldb, ldb * 4, cols * 4, kr,
+                          cudaMemcpyDeviceToDevice, comm->stream) != cudaSuccess)
+      return TM_ERR_CUDA;
+    if (g_nccl.GroupStart() != ncclSuccess) return TM_ERR_NCCL;
+    bool ok = true;
+    if (pc > 1 && rows > 0)
+      ok = g_nccl.Broadcast(Apan, Apan, static_cast<size_t>(rows) * lda_p, ncclFloat32, ja, comm->row_comm,
+                            comm->stream) == ncclSuccess;
+    if (ok && pr > 1 && cols > 0)
+      ok = g_nccl.Broadcast(Bpan, Bpan, static_cast<size_t>(kr) * ldb_p, ncclFloat32, ib, comm->col_comm,
+                            comm->stream) == ncclSuccess;
+    const bool ended = g_nccl.GroupEnd() == ncclSuccess;
+    if (!(ok && ended)) return TM_ERR_NCCL;
+    if (j != ja) comm->bytes_received += static_cast<uint64_t>(rows) * lda_p * 4;
+    if (i != ib) comm->bytes_received += static_cast<uint64_t>(kr) * ldb_p * 4;
+    return TM_OK;
+  };
+  return summa_schedule(pr, pc, r, m, n, k, alpha, beta, C_local, ldc, stream, comm->stream, comm->ev_start,
+                        comm->ev_ready, comm->ev_used, comm->panel_buf, deliver);
+}
+
+tm_status tm_sgemm_summa_loopback(int pr, int pc, int64_t m, int64_t n, int64_t k, float alpha,
+                                  const float* const* A_locals, const int64_t* ldas, const float* const* B_locals,
+                                  const int64_t* ldbs, float beta, float* const* C_locals, const int64_t* ldcs,
+                                  uint64_t* bytes_received, void* stream_) {
+  if (pr < 1 || pc < 1 || !A_locals || !ldas || !B_locals || !ldbs || !C_locals || !ldcs || m < 0 || n < 0 || k < 0)
+    return TM_ERR_INVALID_VALUE;
+  const int P = pr * pc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_ready[2] = {}, ev_used[2] = {};
+  float* buf = nullptr;
+  size_t need = 0;
+  for (int r = 0; r < P; ++r) need = std::max(need, summa_buffer_bytes(pr, pc, r, m, n, k));
+  tm_status st = TM_OK;
+  bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) == cudaSuccess;
+  for (int q = 0; ok && q < 2; ++q)
+    ok = cudaEventCreateWithFlags(&ev_ready[q], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&ev_used[q], cudaEventDisableTiming) == cudaSuccess;
+  if (ok && need) ok = cudaMalloc(&buf, need) == cudaSuccess;
+  if (!ok) st = TM_ERR_CUDA;
+  if (bytes_received)
+    for (int r = 0; r < P; ++r) bytes_received[r] = 0;
+  // Ranks one after another; every rank's panels are packed straight from the
+  // owners' blocks (the broadcast of the NCCL entry point).
+  for (int r = 0; st == TM_OK && r < P; ++r) {
+    const int i = r / pc, j = r % pc;
+    int64_t r0, rows, c0, cols;
+    tm_dist_rows(m, pr, i, &r0, &rows);
+    tm_dist_rows(n, pc, j, &c0, &cols);
+    auto deliver = [&](int, int ja, int64_t ka0, int ib, int64_t kb0, int64_t k0, int64_t kr, float* Apan,
+                       int64_t lda_p, float* Bpan, int64_t ldb_p) -> tm_status {
+      const int oa = i * pc + ja, ob = ib * pc + j;  // owner ranks
+      if (rows > 0 && cudaMemcpy2DAsync(Apan, lda_p * 4, A_locals[oa] + (k0 - ka0), ldas[oa] * 4, kr * 4, rows,
+                                        cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
+        return TM_ERR_CUDA;
+      if (cols > 0 && cudaMemcpy2DAsync(Bpan, ldb_p * 4, B_locals[ob] + (k0 - kb0) * ldbs[ob], ldbs[ob] * 4,
+                                        cols * 4, kr, cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
+        return TM_ERR_CUDA;
+      if (bytes_received) {
+        if (oa != r) bytes_received[r] += static_cast<uint64_t>(rows) * lda_p * 4;
+        if (ob != r) bytes_received[r] += static_cast<uint64_t>(kr) * ldb_p * 4;
+      }
+      return TM_OK;
+    };
+    st = summa_schedule(pr, pc, r, m, n, k, alpha, beta, C_locals[r], ldcs[r], stream, cs, ev_start, ev_ready,
+                        ev_used, buf, deliver);
+    if (st == TM_OK && cudaStreamSynchronize(stream) != cudaSuccess) st = TM_ERR_CUDA;
+  }
+  if (cs) cudaStreamSynchronize(cs);
+  if (buf) cudaFree(buf);
+  for (int q = 0; q < 2; ++q) {
+    if (ev_ready[q]) cudaEventDestroy(ev_ready[q]);
+    if (ev_used[q]) cudaEventDestroy(ev_used[q]);
+  }
   if (ev_start) cudaEventDestroy(ev_start);
   if (cs) cudaStreamDestroy(cs);
   return st;

@@ -1,5 +1,6 @@
-"""The NCCL data plane of the row-sharded mode (tm_comm_*, tm_sgemm_dist,
-tm_sgemm_dist_allgather) on real devices.
+"""The NCCL data plane of the distributed modes (tm_comm_*, tm_sgemm_dist,
+tm_sgemm_dist_fused, tm_sgemm_dist_allgather, tm_sgemm_summa, tm_blur_dist) on
+real devices.
 
 * One rank on the single GPU every box has: tm_comm_init (dlopen of libnccl and
   ncclCommInitRankConfig with the hand-declared ncclConfig_t), tm_comm_check,
@@ -59,6 +60,11 @@ def test_one_rank_comm_lifecycle_and_sgemm():
         assert torch.equal(B_full, dB)
         assert _err(dC2.cpu().numpy(), R, D) <= TOL
         assert comm.bytes_received() == 0  # nothing arrives from other ranks
+        # 2-D SUMMA on a 1 x 1 grid is tm_sgemm
+        dCs = torch.from_numpy(C0).cuda()
+        comm.sgemm_summa(1, 1, m, n, k, dA, dB, dCs, si.ALPHA, si.BETA)
+        torch.cuda.synchronize()
+        assert torch.equal(dCs, ref)
         # the row-distributed blur at P = 1 is tm_blur on the whole image
         N, M = 67, 45
         img = si.image(N, M, seed=64)
@@ -132,6 +138,19 @@ def _worker(rank, world, port, q):
         out["ag_B_equal"] = bool(np.array_equal(B_full.cpu().numpy(), B2))
         out["ag_bytes"] = comm.bytes_received() - before
         out["ag_bytes_expected"] = (world - 1) * kr * n * 4
+        # 2-D SUMMA: pr x pc grid (2 x world/2 when even), panels broadcast along rows / columns
+        pr = 2 if world % 2 == 0 else 1
+        pc = world // pr
+        m3, n3, k3 = 1030, 700, 2600
+        A3, B3, C3 = si.matrices(m3, n3, k3, seed=67)
+        (sr0, srows), (sc0, scols), (sa0, ska), (sb0, skb) = tm.summa_blocks(m3, n3, k3, pr, pc, rank)
+        dA3 = torch.from_numpy(np.ascontiguousarray(A3[sr0:sr0 + srows, sa0:sa0 + ska])).cuda()
+        dB3 = torch.from_numpy(np.ascontiguousarray(B3[sb0:sb0 + skb, sc0:sc0 + scols])).cuda()
+        dC3 = torch.from_numpy(np.ascontiguousarray(C3[sr0:sr0 + srows, sc0:sc0 + scols])).cuda()
+        comm.sgemm_summa(pr, pc, m3, n3, k3, dA3, dB3, dC3, si.ALPHA, si.BETA)
+        torch.cuda.synchronize()
+        R3, D3 = oracle.sgemm(si.ALPHA, A3, B3, si.BETA, C3, rows=np.arange(sr0, sr0 + srows))
+        out["summa_err"] = _err(dC3.cpu().numpy(), R3[:, sc0:sc0 + scols], D3[:, sc0:sc0 + scols])
         # row-distributed blur: border rows from rank + 1 over NCCL
         N, M = 2112, 3520 // 8
         img = si.image(N, M, seed=65)
@@ -182,4 +201,5 @@ def test_multi_rank_nccl_broadcast_and_allgather():
         assert o["bcast_bytes"] == o["bcast_bytes_expected"], o
         assert o["ag_bytes"] == o["ag_bytes_expected"], o
         assert o["blur_err"] <= 1e-6 and o["blur_bytes"] == o["blur_bytes_expected"], o
+        assert o["summa_err"] <= TOL, o
         assert o["check"], o
