@@ -48,6 +48,14 @@
  * closed forms (identity, permutation, all-ones, alpha=0, beta=0 with NaN
  * poison), integer-valued inputs, and a hand-computed golden example
  * (tests/golden/).
+ *
+ * The other functions of this file, each with its own header below and its
+ * own pins: tm_oracle_conv2d_nhwc (the convolution of PAPER.md:824-826;
+ * tests/test_conv_oracle.py), tm_oracle_dist_rows (the row partition,
+ * PAPER.md:503-504; tests/golden/dist_rows.json), tm_oracle_blur (the Blur of
+ * PAPER.md:216-219; tests/test_blur_oracle.py, tests/golden/blur_hand_4x4.json).
+ * tests/test_oracle_mutants.py rebuilds this file with each ORACLE_MUTANT and
+ * requires every mutant to fail a pin.  Every function is pinned.
  */
 #include <math.h>
 #include <stdint.h>
