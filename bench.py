@@ -518,6 +518,11 @@ def run_conv(args):
     paper_default = R == 3 and not args.conv_valid
     traffic, traffic_src = (ncu_traffic("CONV", "tf32x3", 1) if (beta == 0.0 and algo != 2 and paper_default)
                             else (None, None))
+    # Dominant bound: HBM (X, W, Y once) for the 3x3 / 5x5 shapes, the tensor
+    # cores for the large filters (K = R*S*C grows with the filter, the bytes do not)
+    _, tpeak, _, tnote = roofline_peak("tf32x3" if algo != 2 else "simt", peaks)
+    t_hbm, t_tc = algo_bytes / (peaks["hbm_gbs"] * 1e9), flops / (tpeak * 1e12)
+    tensor_bound = t_tc > t_hbm
     line = {"metric": "conv2d GB/s (PAPER.md:826 Conv shape, 3xTF32 tensor cores)", "value": round(gbs, 2), "unit": "GB/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "dtype": "f32 (3xTF32 tensor-core)" if algo != 2 else "f32",
@@ -526,8 +531,13 @@ def run_conv(args):
                                    f"{' (valid)' if args.conv_valid else ''}, alpha {alpha} beta {beta}",
                        "gemm_view": {"m": Nb * Ho * Wo, "n": F, "k": R * S * C},
                        "l2": "inputs larger than L2, no flush"},
-            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
+            "roofline": {"bound": "tensor" if tensor_bound else "hbm",
+                         "achieved": round(flops / (ms * 1e-3) / 1e12, 2) if tensor_bound else round(gbs, 1),
+                         "peak": round(tpeak, 2) if tensor_bound else peaks["hbm_gbs"],
+                         "unit": "TFLOP/s" if tensor_bound else "GB/s",
+                         "frac": round((flops / (ms * 1e-3) / 1e12) / tpeak if tensor_bound else gbs / peaks["hbm_gbs"], 4),
+                         "peak_source": tnote if tensor_bound else peaks["source"] + " hbm_gbs",
+                         "hbm_frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
                          "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
                          "algorithmic_bytes": algo_bytes,
                          "kernel": "k_conv_simt" if algo == 2 else ("k_conv_direct" if R * C <= 128

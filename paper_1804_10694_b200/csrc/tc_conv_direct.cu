@@ -399,13 +399,27 @@ int dc_plan(const ConvArgs& a, DcParams& p) {
   p.bres_bytes = p.stages * p.bbox;
   // TMEM: n_part accumulators of n columns + a_slots A slots of 32 columns per stage
   p.a_cols = p.stages * 2 * kDcBK;
+  // Prefer two accumulators (the epilogue groups alternate tiles) and two A
+  // slots (the split of tile t+1 overlaps the MMAs of tile t); with larger
+  // filters (7x7: N = 112, K = 112 -> A slot of 224 columns) one A slot beside
+  // the two accumulators still beats the implicit-GEMM kernel, whose 49 taps
+  // of 16 channels make 49 small TMA boxes per tile (5.8 ms -> see DESIGN 6.5).
   p.n_part = 2;
   p.a_slots = (512 - 2 * p.n) / p.a_cols;
   if (p.a_slots < 2) {
-    p.n_part = 1;
-    p.a_slots = (512 - p.n) / p.a_cols;
+    const int one_acc = (512 - p.n) / p.a_cols;
+    if (one_acc >= 2) {
+      p.n_part = 1;
+      p.a_slots = one_acc;
+    } else {
+      p.a_slots = (512 - 2 * p.n) / p.a_cols;
+      if (p.a_slots < 1) {
+        p.n_part = 1;
+        p.a_slots = one_acc;
+      }
+    }
   }
-  if (p.a_slots < 2) return 0;
+  if (p.a_slots < 1) return 0;
   if (p.a_slots > kDcMaxSlots) p.a_slots = kDcMaxSlots;
   p.idesc = ptx::idesc_tf32(kDcLanes, p.n, 0, 0);
   const int fixed = 1024 + 2 * p.bres_bytes + kDcEpiWarps * 32 * kEpiStride * 4 + 512;

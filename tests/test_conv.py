@@ -66,11 +66,13 @@ def test_conv_tensor_core_configs(config, shape):
 # Direct kernel geometry: several 128-pixel tiles per output row with a ragged
 # last one, tiles crossing image boundaries, 16/32/48/64 channels (one to
 # three halo boxes, 64-B and 128-B swizzled rows), F below / at / above a
-# power of two, 1x1 .. 5x5 taps with and without padding, one-pixel rows.
+# power of two, 1x1 .. 7x7 taps with and without padding, one-pixel rows.
 DIRECT_SHAPES = [(2, 6, 300, 16, 16, 3, 3, 1), (3, 5, 128, 16, 16, 3, 3, 1), (1, 4, 257, 32, 32, 3, 3, 1),
                  (2, 5, 140, 48, 20, 3, 3, 1), (1, 4, 130, 64, 64, 3, 3, 1), (2, 7, 150, 16, 8, 5, 5, 2),
                  (2, 6, 131, 16, 40, 1, 1, 0), (1, 9, 200, 32, 16, 3, 5, 0), (2, 3, 1, 16, 16, 3, 3, 1),
-                 (1, 40, 3, 16, 12, 3, 1, 1), (1, 9, 140, 16, 16, 3, 7, 3), (2, 6, 133, 16, 24, 5, 5, 2)]
+                 (1, 40, 3, 16, 12, 3, 1, 1), (1, 9, 140, 16, 16, 3, 7, 3), (2, 6, 133, 16, 24, 5, 5, 2),
+                 # 7x7: one TMEM A slot beside two accumulators
+                 (2, 20, 150, 16, 16, 7, 7, 3), (1, 12, 133, 16, 12, 7, 7, 0)]
 
 
 @pytest.mark.parametrize("shape", DIRECT_SHAPES)
