@@ -540,8 +540,10 @@ def run_conv(args):
                          "hbm_frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
                          "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
                          "algorithmic_bytes": algo_bytes,
-                         "kernel": "k_conv_simt" if algo == 2 else ("k_conv_direct" if R * C <= 128
-                                                                    else "k_sgemm_tc<CONV> (implicit GEMM)")},
+                         "kernel": {"direct": "k_conv_direct", "implicit_gemm": "k_sgemm_tc<CONV> (implicit GEMM)",
+                                    "simt": "k_conv_simt"}.get(
+                             tm.conv2d_plan_name(Nb, H, W, C, F, R, S, pad, alpha, algo, X.data_ptr(), Wt.data_ptr(),
+                                                 Y.data_ptr()), "?")},
             "gpu_launches": args.steps,
             "clocks": clocks.summary()}
     print(json.dumps(line), flush=True)

@@ -158,8 +158,10 @@ tm_status tm_sgemm_colmajor(char transa, char transb, int64_t m, int64_t n, int6
  *   Y[b,y,x,f] = alpha * sum_{ky,kx,c} X[b, y+ky-pad, x+kx-pad, c] * Wt[f,ky,kx,c] + beta * Y[b,y,x,f]
  * (X outside the image reads as zero).  AUTO uses a 3xTF32 tensor-core path
  * when c % 16 == 0, f % 4 == 0, pointers 16-byte aligned and pad <= 127 --
- * the direct halo-tile kernel when s is 1, 3, 5 or 7, r * c <= 128 and f <= 64
- * (filters resident in shared memory), else the implicit-GEMM kernel (A =
+ * the direct halo-tile kernel when s is 1, 3, 5, 7 or 9, c <= 128, f <= 64
+ * and the filters fit resident in shared memory (hi and lo: 2 * r * c * 16 *
+ * ceil(f/16) * s * 4 bytes, e.g. 9x9 x 16 channels x 16 filters; larger R are
+ * reduced in passes of filter rows), else the implicit-GEMM kernel (A =
  * im2col of X streamed by TMA im2col-mode copies, never materialised) -- and
  * otherwise the FP32 SIMT direct convolution; TM_ALGO_TF32X3 on shapes
  * outside the tensor-core rule returns TM_ERR_INVALID_VALUE.  Same accuracy contract (normalised by
@@ -167,6 +169,12 @@ tm_status tm_sgemm_colmajor(char transa, char transb, int64_t m, int64_t n, int6
 tm_status tm_conv2d_nhwc(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f, int64_t r, int64_t s,
                          int64_t pad, float alpha, const float* X, const float* Wt, float beta, float* Y,
                          void* stream, int algo);
+
+/* Name of the kernel tm_conv2d_nhwc would run for these arguments ("direct",
+ * "implicit_gemm", "simt", "scale", "noop" or "invalid"); host-only, no
+ * launch (pointers are only inspected for alignment). */
+const char* tm_conv2d_plan_name(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f, int64_t r, int64_t s,
+                                int64_t pad, float alpha, const float* X, const float* Wt, const float* Y, int algo);
 
 /* End-to-end entry with HOST buffers (ideally pinned): copies A, B (and C when
  * beta != 0) to the current device, computes, copies C back, and synchronises

@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = [
     "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_fused", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
     "tm_sgemm_tune", "tm_tune_cache_size", "tm_tune_cache_clear", "tm_tune_cache_save", "tm_tune_cache_load",
     "tm_sgemm_plan_config", "tm_blur", "tm_blur_dist", "tm_blur_dist_loopback",
-    "tm_sgemm_summa", "tm_summa_panel", "tm_sgemm_summa_loopback",
+    "tm_sgemm_summa", "tm_summa_panel", "tm_sgemm_summa_loopback", "tm_conv2d_plan_name",
     "tm_ipc_export", "tm_ce_create", "tm_ce_connect", "tm_ce_destroy", "tm_ce_bytes_received", "tm_sgemm_dist_ce",
 ]
 
@@ -82,6 +82,8 @@ def _load():
     L.tm_blur.argtypes = [i64, i64, vp, i64, vp, i64, vp]
     L.tm_blur_dist.argtypes = [vp, i64, i64, vp, i64, vp, i64, vp]
     L.tm_blur_dist_loopback.argtypes = [ci, i64, i64, vp, i64, vp, i64, vp, vp]
+    L.tm_conv2d_plan_name.argtypes = [i64] * 8 + [f32, vp, vp, vp, ci]
+    L.tm_conv2d_plan_name.restype = ctypes.c_char_p
     L.tm_sgemm_summa.argtypes = [vp, ci, ci, i64, i64, i64, f32, vp, i64, vp, i64, f32, vp, i64, vp]
     L.tm_summa_panel.argtypes = [i64, ci, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.tm_sgemm_summa_loopback.argtypes = [ci, ci, i64, i64, i64, f32, vp, vp, vp, vp, f32, vp, vp, vp, vp]
@@ -93,7 +95,7 @@ def _load():
     L.tm_sgemm_dist_ce.argtypes = [vp, i64, i64, i64, f32, vp, i64, vp, i64, vp, ci, f32, vp, i64, ci, vp]
     for name in EXPORTED_SYMBOLS:
         fn = getattr(L, name)
-        if fn.restype is ctypes.c_int or name in ("tm_status_string", "tm_sgemm_plan_name"):
+        if fn.restype is ctypes.c_int or name in ("tm_status_string", "tm_sgemm_plan_name", "tm_conv2d_plan_name"):
             continue
         fn.restype = ctypes.c_int
     return L
@@ -294,6 +296,13 @@ def conv2d_nhwc(X, Wt, Y, alpha: float = 1.0, beta: float = 0.0, pad: int = 0, a
                             _stream(stream), int(algo))
     _check(st, "tm_conv2d_nhwc")
     return Y
+
+
+def conv2d_plan_name(nb, h, w, c, f, r, s, pad, alpha=1.0, algo=ALGO_AUTO, X_ptr=1 << 20, Wt_ptr=1 << 30,
+                     Y_ptr=1 << 40) -> str:
+    """Host-only: the kernel tm_conv2d_nhwc would run ("direct", "implicit_gemm", "simt", ...)."""
+    return lib.tm_conv2d_plan_name(nb, h, w, c, f, r, s, pad, float(alpha), ctypes.c_void_p(X_ptr),
+                                   ctypes.c_void_p(Wt_ptr), ctypes.c_void_p(Y_ptr), int(algo)).decode()
 
 
 def sgemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None):

@@ -351,6 +351,22 @@ tm_status tm_sgemm(int64_t m, int64_t n, int64_t k, float alpha, const float* A,
   return tm_sgemm_ex(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, stream, TM_ALGO_AUTO);
 }
 
+// The kernel tm_conv2d_nhwc would run (host-only; the same rules).
+const char* tm_conv2d_plan_name(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f, int64_t r, int64_t s,
+                                int64_t pad, float alpha, const float* X, const float* Wt, const float* Y, int algo) {
+  tmk::ConvArgs a{nb, h, w, c, f, r, s, pad, alpha, 0.0f, X, Wt, const_cast<float*>(Y)};
+  if (nb < 0 || h < 1 || w < 1 || c < 1 || f < 1 || r < 1 || s < 1 || pad < 0) return "invalid";
+  if (algo < TM_ALGO_AUTO || algo > TM_ALGO_SIMT_F32 || a.ho() < 1 || a.wo() < 1) return "invalid";
+  if (nb * a.ho() * a.wo() == 0) return "noop";
+  if (alpha == 0.0f) return "scale";
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  const bool tc_ok = (c % 16 == 0) && (f % 4 == 0) && al16(X) && al16(Wt) && al16(Y) && pad <= 127 && r <= 128 &&
+                     s <= 128;
+  if (algo == TM_ALGO_TF32X3 && !tc_ok) return "invalid";
+  if (algo == TM_ALGO_SIMT_F32 || !tc_ok) return "simt";
+  return tmk::conv_direct_fits(a) ? "direct" : "implicit_gemm";
+}
+
 // Implicit-GEMM convolution.
 tm_status tm_conv2d_nhwc(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f, int64_t r, int64_t s, int64_t pad,
                          float alpha, const float* X, const float* Wt, float beta, float* Y, void* stream_, int algo) {

@@ -18,21 +18,28 @@
 // cover halo pixels OW*q .. OW*q + 31 and produce OW = 33 - S outputs, so the
 // shift never crosses a warp.
 //
-// One 4-D tiled TMA box per tile brings the halo -- R input rows x (3 OW + 32)
-// pixels x up to 32 channels, image borders zero-filled by the TMA.  The
-// filters, rearranged by the TMA box itself into B^T rows (f, kx) x 16
-// channels per (ky, 16-channel) stage, stay resident in shared memory, hi and
-// lo, for the whole persistent CTA.
+// The K = R * C reduction runs in PASSES of RPP filter rows (all R rows in one
+// pass when TMEM and shared memory allow; 9x9 takes three passes of 3 rows):
+// one 4-D tiled TMA box per (tile, pass) brings the halo rows of the pass --
+// RPP input rows x (3 OW + 32) pixels x up to 32 channels, image borders
+// zero-filled by the TMA -- and the split writes them into one TMEM A slot;
+// the MMA chain of a tile spans its passes' slots.  The filters, rearranged by
+// the TMA box itself into B^T rows (kx, f) x 16 channels per (ky, 16-channel)
+// stage, stay resident in shared memory, hi and lo, for the whole persistent
+// CTA.  Accumulator column kx * F_pad + f holds Z[., (f, kx)], so the shift-add
+// reads 16 filters of one kx per TMEM load, whatever S.
 //
 // Warp roles (512 threads, one CTA per SM, persistent over tiles):
 //   warps 0, 2     halo producers (one lane each, alternate tiles); warp 0
 //                  also loads the filters once.  Warp 2 allocates TMEM.
 //   warp 1         MMA issuer (one lane).
-//   warps 4-7      split: halo -> (hi | lo) TMEM A slots, one slot per tile.
+//   warps 4-7      split: halo -> (hi | lo) TMEM A slots, one slot per (tile, pass).
 //   warps 8-15     promotion, shift-add and epilogue, two warpgroups, one per
 //                  TMEM accumulator (tc_gemm.cuh epi_store: alpha / beta,
 //                  full / partial tile separation).  The epilogue is the
 //                  longest per-tile chain, hence two groups.
+#include <algorithm>
+
 #include "tc_gemm.cuh"
 
 namespace tmk {
@@ -43,7 +50,7 @@ constexpr int kDcLanes = 128;        // halo pixels per tile = TMEM lanes
 constexpr int kDcSplitWarps = 4;     // one split warpgroup
 constexpr int kDcEpiWarps = 8;       // two promotion / epilogue warpgroups (one per accumulator)
 constexpr int kDcMaxSlots = 4;       // TMEM A slots (one tile each)
-constexpr int kDcMaxStages = 8;      // R * C / 16 (K = R * C <= 128)
+constexpr int kDcMaxStages = 8;      // stages (16-channel rows) per pass: RPP * C / 16
 constexpr int kDcMaxSmem = 227 * 1024;
 // The halo producers alternate tiles by parity and the halo ring depth is
 // even, so every ring slot is always filled by the same producer: each slot's
@@ -57,15 +64,17 @@ struct DcParams {
   int ow;              // outputs per warp = 33 - S
   int tiles_x, num_tiles;
   int chunks;          // c / 16
-  int stages;          // r * chunks: K = 16 * stages <= 128
+  int stages;          // r * chunks: K = 16 * stages (resident filter stages)
+  int rpp, passes;     // filter rows per pass, passes per tile (last may be shorter)
+  int pstages;         // stages of a full pass: rpp * chunks <= kDcMaxStages
   int cw;              // channels per halo box (16 or 32)
   int halo_w;          // 3 * ow + 32 pixels
-  int box_bytes;       // one halo box (r x halo_w x cw floats), 1 KiB aligned
+  int box_bytes;       // one halo box (rpp x halo_w x cw floats), 1 KiB aligned
   int slot_bytes;      // (c / cw) boxes
   int n_slots;         // halo ring depth
   int bbox;            // one filter stage box: n rows x 64 B
   int bres_bytes;      // resident filters, hi (same again for lo)
-  int a_slots, a_cols; // TMEM A ring: slots of a_cols = stages * 32 columns
+  int a_slots, a_cols; // TMEM A ring: slots of a_cols = pstages * 32 columns
   int n_part;          // TMEM accumulators (n columns each)
   uint32_t idesc;
   float alpha, beta;
@@ -139,22 +148,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.stages * p.bbox));
           for (int s = 0; s < p.stages; ++s) {
             const int ky = s / p.chunks, ci = s - ky * p.chunks;
-            ptx::tma_load_4d(bres + s * p.bbox, &tmW, bres_full, ci * kDcBK, 0, ky, 0);
+            ptx::tma_load_4d(bres + s * p.bbox, &tmW, bres_full, ci * kDcBK, 0, 0, ky);
           }
         }
         int slot = 0, own = 0;
         uint32_t ph = 0;
         const int boxes = p.c / p.cw;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x)
+        for (int ps = 0; ps < p.passes; ++ps) {
           if (own == pi) {
             int b, y, x0;
             dc_tile(p, t, b, y, x0);
             ptx::mbar_wait(&halo_empty[slot], ph ^ 1);
-            ptx::mbar_arrive_expect_tx(&halo_full[slot], static_cast<uint32_t>(boxes * p.r * p.halo_w * p.cw * 4));
+            ptx::mbar_arrive_expect_tx(&halo_full[slot], static_cast<uint32_t>(boxes * p.rpp * p.halo_w * p.cw * 4));
             for (int i = 0; i < boxes; ++i)
               ptx::tma_load_4d(halo + slot * p.slot_bytes + i * p.box_bytes, &tmX, &halo_full[slot], i * p.cw,
-                               x0 - p.pad, y - p.pad, b);
-            if (p.beta != 0.0f) {
+                               x0 - p.pad, y - p.pad + ps * p.rpp, b);
+            if (p.beta != 0.0f && ps == 0) {
               // the epilogue will read beta * Y for this tile's outputs (one
               // contiguous run of the output row): stage it in L2 now, the
               // halo ring depth ahead of its use
@@ -178,25 +188,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phl = 0, pph = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         ptx::mbar_wait(&part_empty[pb], pph ^ 1);
-        ptx::mbar_wait(&ready[sl], phl);
-        ptx::tc_fence_after();
         const uint32_t d = tmem_base + static_cast<uint32_t>(pb * p.n);
-        uint32_t a = tmem_base + acol + static_cast<uint32_t>(sl * p.a_cols);
         uint32_t boff = 0;
-        for (int s = 0; s < p.stages; ++s) {
+        int sg = 0;  // filter stage (global over the passes)
+        for (int ps = 0; ps < p.passes; ++ps) {
+          ptx::mbar_wait(&ready[sl], phl);
+          ptx::tc_fence_after();
+          uint32_t a = tmem_base + acol + static_cast<uint32_t>(sl * p.a_cols);
+          const int ns = min(p.pstages, p.stages - sg);
+          for (int s = 0; s < ns; ++s, ++sg) {
 #pragma unroll
-          for (int ks = 0; ks < kDcBK / 8; ++ks) {
-            const uint64_t bH = bH0 + boff + 2 * ks, bL = bL0 + boff + 2 * ks;  // +32 B per K step of 8
-            ptx::mma_tf32_tmem_a<1>(d, a + kDcBK + 8 * ks, bH, idesc, (s | ks) ? 1u : 0u);  // A_lo B_hi
-            ptx::mma_tf32_tmem_a<1>(d, a + 8 * ks, bL, idesc, 1u);                         // A_hi B_lo
-            ptx::mma_tf32_tmem_a<1>(d, a + 8 * ks, bH, idesc, 1u);                         // A_hi B_hi
+            for (int ks = 0; ks < kDcBK / 8; ++ks) {
+              const uint64_t bH = bH0 + boff + 2 * ks, bL = bL0 + boff + 2 * ks;  // +32 B per K step of 8
+              ptx::mma_tf32_tmem_a<1>(d, a + kDcBK + 8 * ks, bH, idesc, (sg | ks) ? 1u : 0u);  // A_lo B_hi
+              ptx::mma_tf32_tmem_a<1>(d, a + 8 * ks, bL, idesc, 1u);                          // A_hi B_lo
+              ptx::mma_tf32_tmem_a<1>(d, a + 8 * ks, bH, idesc, 1u);                          // A_hi B_hi
+            }
+            a += 2 * kDcBK;
+            boff += bstep;
           }
-          a += 2 * kDcBK;
-          boff += bstep;
+          ptx::mma_commit<1>(&a_empty[sl]);
+          if (++sl == p.a_slots) { sl = 0; phl ^= 1; }
         }
-        ptx::mma_commit<1>(&a_empty[sl]);
         ptx::mma_commit<1>(&part_full[pb]);
-        if (++sl == p.a_slots) { sl = 0; phl ^= 1; }
         if (++pb == p.n_part) { pb = 0; pph ^= 1; }
       }
     }
@@ -224,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t soff[kDcMaxStages], sxor[kDcMaxStages];
 #pragma unroll
     for (int s = 0; s < kDcMaxStages; ++s) {
-      const int ky = s / p.chunks, ci = s - ky * p.chunks;
+      const int ky = s / p.chunks, ci = s - ky * p.chunks;  // row within the pass
       const int box = cw16 ? ci : (ci >> 1);
       const int within = cw16 ? 0 : ((ci & 1) << 2);  // first 16-B chunk of these 16 channels
       const int row = ky * p.halo_w + hp;             // pixel row inside the box
@@ -232,10 +246,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       sxor[s] = static_cast<uint32_t>(cw16 ? ((row >> 1) & 3) : (row & 7));
       sxor[s] = (sxor[s] ^ static_cast<uint32_t>(within)) & 7u;  // within in {0, 4} and j < 4: (within + j) ^ sw = (j ^ (sw ^ within))
     }
-    int slot = 0, sl = 0, i = 0;
+    int slot = 0, sl = 0;
     uint32_t ph = 0, phl = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x)
+    for (int ps = 0; ps < p.passes; ++ps) {
       {
+        const int ns = min(p.pstages, p.stages - ps * p.pstages);
         ptx::mbar_wait(&halo_full[slot], ph);
         ptx::mbar_wait(&a_empty[sl], phl ^ 1);
         ptx::tc_fence_after();
@@ -243,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ta = trow + static_cast<uint32_t>(sl * p.a_cols);
 #pragma unroll
         for (int s = 0; s < kDcMaxStages; ++s) {
-          if (s >= p.stages) break;
+          if (s >= ns) break;
           const uint32_t rowp = hb + soff[s];
           uint4 v[4];
 #pragma unroll
@@ -296,24 +312,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = (b * p.ho + y) * p.wo + xw;         // its GEMM row (output pixel index)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(pb * p.n);
       for (int f0 = 0; f0 < p.fp; f0 += 16) {
-        // columns (f, kx) for f in [f0, f0 + 16): 16 * S consecutive columns
-        uint32_t r[16 * S];
-#pragma unroll
-        for (int c = 0; c < S; ++c)
-          ptx::tmem_ld_32x32b_x16(taddr + f0 * S + 16 * c, *reinterpret_cast<uint32_t(*)[16]>(r + 16 * c));
-        ptx::tmem_ld_wait();
-        if (f0 + 16 >= p.fp) {  // last read of this accumulator: hand it back to the MMA
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&part_empty[pb]);
-        }
+        // column kx * fp + f holds Z[., (f, kx)]: per kx, 16 consecutive columns
+        // of filters f0 .. f0 + 15; loads in groups of KG taps (registers)
+        constexpr int KG = S <= 7 ? S : (S + 1) / 2;
         float acc[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float v = __uint_as_float(r[j * S]);  // kx = 0
+        for (int k0 = 0; k0 < S; k0 += KG) {
+          uint32_t r[16 * KG];
 #pragma unroll
-          for (int kx = 1; kx < S; ++kx) v += __shfl_down_sync(0xffffffffu, __uint_as_float(r[j * S + kx]), kx);
-          acc[j] = v;
+          for (int c = 0; c < KG; ++c)
+            if (k0 + c < S)
+              ptx::tmem_ld_32x32b_x16(taddr + (k0 + c) * p.fp + f0, *reinterpret_cast<uint32_t(*)[16]>(r + 16 * c));
+          ptx::tmem_ld_wait();
+          if (f0 + 16 >= p.fp && k0 + KG >= S) {  // last read of this accumulator: hand it back to the MMA
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&part_empty[pb]);
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+#pragma unroll
+            for (int c = 0; c < KG; ++c) {
+              const int kx = k0 + c;
+              if (kx >= S) continue;
+              if (kx == 0) acc[j] = __uint_as_float(r[j]);  // kx = 0, then kx ascending
+              else acc[j] += __shfl_down_sync(0xffffffffu, __uint_as_float(r[16 * c + j]), kx);
+            }
+          }
         }
         if (valid > 0 && f0 < p.f)
           epi_store<16>(p.Y, p.f, row0 + valid, p.f, row0, f0, acc, p.alpha, p.beta, stage, lane);
@@ -331,14 +356,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // NHWC input {C, W, H, N}, box {cw, halo_w, r, 1}: one tile's input rows.
-bool encode_halo(CUtensorMap* map, const ConvArgs& a, int cw, int halo_w) {
+bool encode_halo(CUtensorMap* map, const ConvArgs& a, int cw, int halo_w, int rows) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.c), static_cast<cuuint64_t>(a.w), static_cast<cuuint64_t>(a.h),
                         static_cast<cuuint64_t>(a.nb)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(a.c) * 4, static_cast<cuuint64_t>(a.c * a.w) * 4,
                            static_cast<cuuint64_t>(a.c * a.w * a.h) * 4};
-  cuuint32_t box[4] = {static_cast<cuuint32_t>(cw), static_cast<cuuint32_t>(halo_w), static_cast<cuuint32_t>(a.r), 1};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(cw), static_cast<cuuint32_t>(halo_w), static_cast<cuuint32_t>(rows), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(a.X), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, cw == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
@@ -346,16 +371,17 @@ bool encode_halo(CUtensorMap* map, const ConvArgs& a, int cw, int halo_w) {
   return r == CUDA_SUCCESS;
 }
 
-// KRSC filters {C, S, R, F}, box {16, S, 1, fp}: rows (f, kx) of one (ky, 16
-// channels) stage; filters f >= F are zero-filled.
+// KRSC filters as {C, F, S, R} (strides of the KRSC tensor reordered), box
+// {16, fp, S, 1}: rows (kx, f) of one (ky, 16 channels) stage -- B^T row
+// kx * fp + f; filters f >= F are zero-filled.
 bool encode_filters(CUtensorMap* map, const ConvArgs& a, int fp) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.c), static_cast<cuuint64_t>(a.s), static_cast<cuuint64_t>(a.r),
-                        static_cast<cuuint64_t>(a.f)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(a.c) * 4, static_cast<cuuint64_t>(a.c * a.s) * 4,
-                           static_cast<cuuint64_t>(a.c * a.s * a.r) * 4};
-  cuuint32_t box[4] = {static_cast<cuuint32_t>(kDcBK), static_cast<cuuint32_t>(a.s), 1, static_cast<cuuint32_t>(fp)};
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.c), static_cast<cuuint64_t>(a.f), static_cast<cuuint64_t>(a.s),
+                        static_cast<cuuint64_t>(a.r)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(a.c * a.s * a.r) * 4, static_cast<cuuint64_t>(a.c) * 4,
+                           static_cast<cuuint64_t>(a.c * a.s) * 4};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(kDcBK), static_cast<cuuint32_t>(fp), static_cast<cuuint32_t>(a.s), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(a.Wt), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -364,10 +390,14 @@ bool encode_filters(CUtensorMap* map, const ConvArgs& a, int fp) {
 }
 
 // Fills p and returns the dynamic shared-memory size, or 0 if the shape does
-// not fit the direct kernel (then the implicit-GEMM kernel runs).
+// not fit the direct kernel (then the implicit-GEMM kernel runs).  Passes:
+// the largest RPP (filter rows per pass) for which two TMEM A slots fit beside
+// the accumulators and the halo ring fits in shared memory, else the largest
+// with one A slot; the resident filters (all R*C/16 stages, hi and lo) must
+// fit in any case -- 9x9 x 16 channels does (166 KB), 11x11 does not.
 int dc_plan(const ConvArgs& a, DcParams& p) {
-  if (a.s != 1 && a.s != 3 && a.s != 5 && a.s != 7) return 0;
-  if (a.c % kDcBK != 0 || a.r * a.c > 128 || a.f > 64 || a.r > 8) return 0;
+  if (a.s != 1 && a.s != 3 && a.s != 5 && a.s != 7 && a.s != 9) return 0;
+  if (a.c % kDcBK != 0 || a.f > 64 || a.r < 1) return 0;
   const int64_t ho = a.ho(), wo = a.wo();
   if (ho <= 0 || wo <= 0) return 0;
   p = DcParams{};
@@ -390,41 +420,40 @@ int dc_plan(const ConvArgs& a, DcParams& p) {
   if (tiles > INT32_MAX / 2 || a.nb * ho * wo > INT32_MAX / 2) return 0;
   p.num_tiles = static_cast<int>(tiles);
   p.chunks = p.c / kDcBK;
+  if (p.chunks > kDcMaxStages) return 0;
   p.stages = p.r * p.chunks;
   p.cw = p.c % 32 == 0 ? 32 : 16;
   p.halo_w = 3 * p.ow + 32;
-  p.box_bytes = (p.r * p.halo_w * p.cw * 4 + 1023) / 1024 * 1024;
-  p.slot_bytes = (p.c / p.cw) * p.box_bytes;
   p.bbox = p.n * kDcBK * 4;
   p.bres_bytes = p.stages * p.bbox;
-  // TMEM: n_part accumulators of n columns + a_slots A slots of 32 columns per stage
-  p.a_cols = p.stages * 2 * kDcBK;
-  // Prefer two accumulators (the epilogue groups alternate tiles) and two A
-  // slots (the split of tile t+1 overlaps the MMAs of tile t); with larger
-  // filters (7x7: N = 112, K = 112 -> A slot of 224 columns) one A slot beside
-  // the two accumulators still beats the implicit-GEMM kernel, whose 49 taps
-  // of 16 channels make 49 small TMA boxes per tile (5.8 ms -> see DESIGN 6.5).
-  p.n_part = 2;
-  p.a_slots = (512 - 2 * p.n) / p.a_cols;
-  if (p.a_slots < 2) {
-    const int one_acc = (512 - p.n) / p.a_cols;
-    if (one_acc >= 2) {
-      p.n_part = 1;
-      p.a_slots = one_acc;
-    } else {
-      p.a_slots = (512 - 2 * p.n) / p.a_cols;
-      if (p.a_slots < 1) {
-        p.n_part = 1;
-        p.a_slots = one_acc;
-      }
+  const int fixed = 1024 + 2 * p.bres_bytes + kDcEpiWarps * 32 * kEpiStride * 4 + 512;
+  if (fixed >= kDcMaxSmem) return 0;
+  int best_rpp = 0, best_slots = 0, best_part = 0;
+  for (int want_slots = 2; want_slots >= 1 && !best_rpp; --want_slots) {
+    for (int rpp = std::min(p.r, kDcMaxStages / p.chunks); rpp >= 1; --rpp) {
+      const int a_cols = rpp * p.chunks * 2 * kDcBK;
+      int part = 2, slots = (512 - 2 * p.n) / a_cols;
+      if (slots < want_slots) { part = 1; slots = (512 - p.n) / a_cols; }
+      if (slots < want_slots) continue;
+      const int box = (rpp * p.halo_w * p.cw * 4 + 1023) / 1024 * 1024;
+      if ((kDcMaxSmem - fixed) / ((p.c / p.cw) * box) < 2) continue;
+      best_rpp = rpp;
+      best_slots = slots;
+      best_part = part;
+      break;
     }
   }
-  if (p.a_slots < 1) return 0;
-  if (p.a_slots > kDcMaxSlots) p.a_slots = kDcMaxSlots;
+  if (!best_rpp) return 0;
+  p.rpp = best_rpp;
+  p.passes = (p.r + p.rpp - 1) / p.rpp;
+  p.pstages = p.rpp * p.chunks;
+  p.a_cols = p.pstages * 2 * kDcBK;
+  p.n_part = best_part;
+  p.a_slots = best_slots > kDcMaxSlots ? kDcMaxSlots : best_slots;
+  p.box_bytes = (p.rpp * p.halo_w * p.cw * 4 + 1023) / 1024 * 1024;
+  p.slot_bytes = (p.c / p.cw) * p.box_bytes;
   p.idesc = ptx::idesc_tf32(kDcLanes, p.n, 0, 0);
-  const int fixed = 1024 + 2 * p.bres_bytes + kDcEpiWarps * 32 * kEpiStride * 4 + 512;
   const int slots = (kDcMaxSmem - fixed) / p.slot_bytes;
-  if (slots < 2) return 0;
   p.n_slots = slots < 4 ? (slots & ~1) : 4;  // even (see kDcProducers)
   p.alpha = a.alpha;
   p.beta = a.beta;
@@ -435,7 +464,7 @@ int dc_plan(const ConvArgs& a, DcParams& p) {
 template <int S>
 tm_status launch_dc(const ConvArgs& a, const DcParams& p, int smem, int num_sms, cudaStream_t stream) {
   CUtensorMap tmX, tmW;
-  if (!encode_halo(&tmX, a, p.cw, p.halo_w)) return TM_ERR_INTERNAL;
+  if (!encode_halo(&tmX, a, p.cw, p.halo_w, p.rpp)) return TM_ERR_INTERNAL;
   if (!encode_filters(&tmW, a, p.fp)) return TM_ERR_INTERNAL;
   auto kern = k_conv_direct<S>;
   static std::atomic<unsigned long long> optin{0};  // per instantiation, bit per device
@@ -460,7 +489,8 @@ tm_status launch_conv_direct(const ConvArgs& a, int num_sms, cudaStream_t stream
     case 1: return launch_dc<1>(a, p, smem, num_sms, stream);
     case 3: return launch_dc<3>(a, p, smem, num_sms, stream);
     case 5: return launch_dc<5>(a, p, smem, num_sms, stream);
-    default: return launch_dc<7>(a, p, smem, num_sms, stream);
+    case 7: return launch_dc<7>(a, p, smem, num_sms, stream);
+    default: return launch_dc<9>(a, p, smem, num_sms, stream);
   }
 }
 

@@ -191,3 +191,15 @@ def test_blur_invalid_arguments_rejected_on_host(args):
 def test_blur_dist_loopback_rejects_bad_rank_count_on_host():
     P = (ctypes.c_void_p * 1)(1 << 20)
     assert tm.lib.tm_blur_dist_loopback(0, 9, 9, P, 27, P, 21, None, None) == 1
+
+
+def test_conv_plan_names_for_the_paper_filter_sizes():
+    """PAPER.md:834-835 (3x3 ... 11x11 on 32x512x512x16, 16 filters): the direct
+    kernel takes 3x3 .. 9x9 (9x9 in passes of filter rows), 11x11's resident
+    filters (2 x 11 x 176 x 64 B) exceed shared memory -> implicit GEMM;
+    channels not a multiple of 16 -> SIMT; host-only."""
+    for r, want in ((1, "direct"), (3, "direct"), (5, "direct"), (7, "direct"), (9, "direct"), (11, "implicit_gemm")):
+        assert tm.conv2d_plan_name(32, 512, 512, 16, 16, r, r, r // 2) == want, r
+    assert tm.conv2d_plan_name(1, 8, 8, 18, 16, 3, 3, 1) == "simt"
+    assert tm.conv2d_plan_name(1, 8, 8, 16, 16, 3, 3, 1, alpha=0.0) == "scale"
+    assert tm.conv2d_plan_name(1, 2, 2, 16, 16, 3, 3, 0) == "invalid"  # no output pixel
