@@ -158,10 +158,11 @@ tm_status tm_sgemm_colmajor(char transa, char transb, int64_t m, int64_t n, int6
  *   Y[b,y,x,f] = alpha * sum_{ky,kx,c} X[b, y+ky-pad, x+kx-pad, c] * Wt[f,ky,kx,c] + beta * Y[b,y,x,f]
  * (X outside the image reads as zero).  AUTO uses a 3xTF32 tensor-core path
  * when c % 16 == 0, f % 4 == 0, pointers 16-byte aligned and pad <= 127 --
- * the direct halo-tile kernel when s is 1, 3, 5, 7 or 9, c <= 128, f <= 64
- * and the filters fit resident in shared memory (hi and lo: 2 * r * c * 16 *
- * ceil(f/16) * s * 4 bytes, e.g. 9x9 x 16 channels x 16 filters; larger R are
- * reduced in passes of filter rows), else the implicit-GEMM kernel (A =
+ * the direct halo-tile kernel when s <= 24, c <= 128 and f <= 64 (the
+ * reduction over filter rows runs in passes; filters whose resident hi + lo
+ * copies exceed shared memory, e.g. 11x11 x 16 channels, are split over two
+ * launches by filter column, the second accumulating with beta = 1; see
+ * tm_conv2d_plan_name), else the implicit-GEMM kernel (A =
  * im2col of X streamed by TMA im2col-mode copies, never materialised) -- and
  * otherwise the FP32 SIMT direct convolution; TM_ALGO_TF32X3 on shapes
  * outside the tensor-core rule returns TM_ERR_INVALID_VALUE.  Same accuracy contract (normalised by

@@ -60,8 +60,9 @@ constexpr int kDcProducers = 2;
 struct DcParams {
   int nb, h, w, c, f, r, pad, ho, wo;
   int fp;              // filters padded to a multiple of 16
-  int n;               // MMA N = fp * S
-  int ow;              // outputs per warp = 33 - S
+  int n;               // MMA N = fp * S (S: the taps of this launch)
+  int ow;              // outputs per warp = 33 - (full filter width)
+  int kx0;             // first filter column kx of this launch (kx split: 0, then S of the first)
   int tiles_x, num_tiles;
   int chunks;          // c / 16
   int stages;          // r * chunks: K = 16 * stages (resident filter stages)
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.stages * p.bbox));
           for (int s = 0; s < p.stages; ++s) {
             const int ky = s / p.chunks, ci = s - ky * p.chunks;
-            ptx::tma_load_4d(bres + s * p.bbox, &tmW, bres_full, ci * kDcBK, 0, 0, ky);
+            ptx::tma_load_4d(bres + s * p.bbox, &tmW, bres_full, ci * kDcBK, 0, p.kx0, ky);
           }
         }
         int slot = 0, own = 0;
@@ -335,8 +336,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < KG; ++c) {
               const int kx = k0 + c;
               if (kx >= S) continue;
-              if (kx == 0) acc[j] = __uint_as_float(r[j]);  // kx = 0, then kx ascending
-              else acc[j] += __shfl_down_sync(0xffffffffu, __uint_as_float(r[16 * c + j]), kx);
+              // tap p.kx0 + kx of output lane x sits in halo lane x + p.kx0 + kx
+              const float z = __shfl_down_sync(0xffffffffu, __uint_as_float(r[16 * c + j]), p.kx0 + kx);
+              if (kx == 0) acc[j] = z;  // first tap, then kx ascending
+              else acc[j] += z;
             }
           }
         }
@@ -372,16 +375,17 @@ bool encode_halo(CUtensorMap* map, const ConvArgs& a, int cw, int halo_w, int ro
 }
 
 // KRSC filters as {C, F, S, R} (strides of the KRSC tensor reordered), box
-// {16, fp, S, 1}: rows (kx, f) of one (ky, 16 channels) stage -- B^T row
-// kx * fp + f; filters f >= F are zero-filled.
-bool encode_filters(CUtensorMap* map, const ConvArgs& a, int fp) {
+// {16, fp, taps, 1}: rows (kx, f) of one (ky, 16 channels) stage -- B^T row
+// (kx - kx0) * fp + f for the launch's taps kx0 .. kx0 + taps - 1; filters
+// f >= F are zero-filled.
+bool encode_filters(CUtensorMap* map, const ConvArgs& a, int fp, int taps) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.c), static_cast<cuuint64_t>(a.f), static_cast<cuuint64_t>(a.s),
                         static_cast<cuuint64_t>(a.r)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(a.c * a.s * a.r) * 4, static_cast<cuuint64_t>(a.c) * 4,
                            static_cast<cuuint64_t>(a.c * a.s) * 4};
-  cuuint32_t box[4] = {static_cast<cuuint32_t>(kDcBK), static_cast<cuuint32_t>(fp), static_cast<cuuint32_t>(a.s), 1};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(kDcBK), static_cast<cuuint32_t>(fp), static_cast<cuuint32_t>(taps), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(a.Wt), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -395,8 +399,8 @@ bool encode_filters(CUtensorMap* map, const ConvArgs& a, int fp) {
 // the accumulators and the halo ring fits in shared memory, else the largest
 // with one A slot; the resident filters (all R*C/16 stages, hi and lo) must
 // fit in any case -- 9x9 x 16 channels does (166 KB), 11x11 does not.
-int dc_plan(const ConvArgs& a, DcParams& p) {
-  if (a.s != 1 && a.s != 3 && a.s != 5 && a.s != 7 && a.s != 9) return 0;
+int dc_plan(const ConvArgs& a, DcParams& p, int kx0, int taps) {
+  if (a.s > 32 - 8 || taps < 1 || taps > 9 || kx0 < 0 || kx0 + taps > a.s) return 0;
   if (a.c % kDcBK != 0 || a.f > 64 || a.r < 1) return 0;
   const int64_t ho = a.ho(), wo = a.wo();
   if (ho <= 0 || wo <= 0) return 0;
@@ -410,11 +414,11 @@ int dc_plan(const ConvArgs& a, DcParams& p) {
   p.pad = static_cast<int>(a.pad);
   p.ho = static_cast<int>(ho);
   p.wo = static_cast<int>(wo);
-  const int s = static_cast<int>(a.s);
   p.fp = (p.f + 15) / 16 * 16;
-  p.n = p.fp * s;
+  p.n = p.fp * taps;
   if (p.n > 256) return 0;
-  p.ow = 33 - s;
+  p.ow = 33 - static_cast<int>(a.s);
+  p.kx0 = kx0;
   p.tiles_x = static_cast<int>((wo + 4 * p.ow - 1) / (4 * p.ow));
   const int64_t tiles = a.nb * ho * p.tiles_x;
   if (tiles > INT32_MAX / 2 || a.nb * ho * wo > INT32_MAX / 2) return 0;
@@ -465,7 +469,7 @@ template <int S>
 tm_status launch_dc(const ConvArgs& a, const DcParams& p, int smem, int num_sms, cudaStream_t stream) {
   CUtensorMap tmX, tmW;
   if (!encode_halo(&tmX, a, p.cw, p.halo_w, p.rpp)) return TM_ERR_INTERNAL;
-  if (!encode_filters(&tmW, a, p.fp)) return TM_ERR_INTERNAL;
+  if (!encode_filters(&tmW, a, p.fp, S)) return TM_ERR_INTERNAL;
   auto kern = k_conv_direct<S>;
   static std::atomic<unsigned long long> optin{0};  // per instantiation, bit per device
   if (tm_status st = ensure_smem_optin(optin, kern, kDcMaxSmem); st != TM_OK) return st;
@@ -476,22 +480,52 @@ tm_status launch_dc(const ConvArgs& a, const DcParams& p, int smem, int num_sms,
 
 }  // namespace
 
+// The direct kernel takes the whole filter width in one launch when its
+// resident filters fit; otherwise (11x11 x 16 channels: 248 KB of hi + lo
+// filters) the filter columns are split in two launches, kx in [0, S1) and
+// [S1, S): the second adds its taps to the first's result (beta = 1), at the
+// cost of reading X twice and Y once more -- the tensor work, which bounds
+// these shapes, is unchanged.
+static bool dc_split(const ConvArgs& a, DcParams& p1, int& s1, DcParams& p2, int& s2, int& smem1, int& smem2) {
+  s1 = static_cast<int>(a.s);
+  s2 = 0;
+  if ((smem1 = dc_plan(a, p1, 0, s1)) > 0) return true;
+  s1 = static_cast<int>((a.s + 1) / 2);
+  s2 = static_cast<int>(a.s) - s1;
+  smem1 = dc_plan(a, p1, 0, s1);
+  smem2 = dc_plan(a, p2, s1, s2);
+  return smem1 > 0 && smem2 > 0;
+}
+
 bool conv_direct_fits(const ConvArgs& a) {
-  DcParams p;
-  return dc_plan(a, p) > 0;
+  DcParams p1, p2;
+  int s1, s2, m1, m2;
+  return dc_split(a, p1, s1, p2, s2, m1, m2);
+}
+
+static tm_status launch_taps(const ConvArgs& a, const DcParams& p, int taps, int smem, int num_sms, cudaStream_t stream) {
+  switch (taps) {
+    case 1: return launch_dc<1>(a, p, smem, num_sms, stream);
+    case 2: return launch_dc<2>(a, p, smem, num_sms, stream);
+    case 3: return launch_dc<3>(a, p, smem, num_sms, stream);
+    case 4: return launch_dc<4>(a, p, smem, num_sms, stream);
+    case 5: return launch_dc<5>(a, p, smem, num_sms, stream);
+    case 6: return launch_dc<6>(a, p, smem, num_sms, stream);
+    case 7: return launch_dc<7>(a, p, smem, num_sms, stream);
+    case 8: return launch_dc<8>(a, p, smem, num_sms, stream);
+    case 9: return launch_dc<9>(a, p, smem, num_sms, stream);
+    default: return TM_ERR_INVALID_VALUE;
+  }
 }
 
 tm_status launch_conv_direct(const ConvArgs& a, int num_sms, cudaStream_t stream) {
-  DcParams p;
-  const int smem = dc_plan(a, p);
-  if (smem == 0) return TM_ERR_INVALID_VALUE;
-  switch (a.s) {
-    case 1: return launch_dc<1>(a, p, smem, num_sms, stream);
-    case 3: return launch_dc<3>(a, p, smem, num_sms, stream);
-    case 5: return launch_dc<5>(a, p, smem, num_sms, stream);
-    case 7: return launch_dc<7>(a, p, smem, num_sms, stream);
-    default: return launch_dc<9>(a, p, smem, num_sms, stream);
-  }
+  DcParams p1, p2;
+  int s1, s2, m1, m2;
+  if (!dc_split(a, p1, s1, p2, s2, m1, m2)) return TM_ERR_INVALID_VALUE;
+  tm_status st = launch_taps(a, p1, s1, m1, num_sms, stream);
+  if (st != TM_OK || s2 == 0) return st;
+  p2.beta = 1.0f;  // add the remaining taps to the first launch's result
+  return launch_taps(a, p2, s2, m2, num_sms, stream);
 }
 
 }  // namespace tmk

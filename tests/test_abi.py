@@ -195,10 +195,12 @@ def test_blur_dist_loopback_rejects_bad_rank_count_on_host():
 
 def test_conv_plan_names_for_the_paper_filter_sizes():
     """PAPER.md:834-835 (3x3 ... 11x11 on 32x512x512x16, 16 filters): the direct
-    kernel takes 3x3 .. 9x9 (9x9 in passes of filter rows), 11x11's resident
-    filters (2 x 11 x 176 x 64 B) exceed shared memory -> implicit GEMM;
+    kernel takes all of them (9x9 in passes of filter rows; 11x11, whose
+    resident filters would need 2 x 11 x 176 x 64 B, in two launches over the
+    filter columns); 25x25 does not fit a warp's shift -> implicit GEMM;
     channels not a multiple of 16 -> SIMT; host-only."""
-    for r, want in ((1, "direct"), (3, "direct"), (5, "direct"), (7, "direct"), (9, "direct"), (11, "implicit_gemm")):
+    assert tm.conv2d_plan_name(1, 64, 64, 16, 16, 25, 25, 12) == "implicit_gemm"
+    for r, want in ((1, "direct"), (3, "direct"), (5, "direct"), (7, "direct"), (9, "direct"), (11, "direct")):
         assert tm.conv2d_plan_name(32, 512, 512, 16, 16, r, r, r // 2) == want, r
     assert tm.conv2d_plan_name(1, 8, 8, 18, 16, 3, 3, 1) == "simt"
     assert tm.conv2d_plan_name(1, 8, 8, 16, 16, 3, 3, 1, alpha=0.0) == "scale"

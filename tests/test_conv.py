@@ -72,7 +72,10 @@ DIRECT_SHAPES = [(2, 6, 300, 16, 16, 3, 3, 1), (3, 5, 128, 16, 16, 3, 3, 1), (1,
                  (2, 6, 131, 16, 40, 1, 1, 0), (1, 9, 200, 32, 16, 3, 5, 0), (2, 3, 1, 16, 16, 3, 3, 1),
                  (1, 40, 3, 16, 12, 3, 1, 1), (1, 9, 140, 16, 16, 3, 7, 3), (2, 6, 133, 16, 24, 5, 5, 2),
                  # 7x7: one TMEM A slot beside two accumulators
-                 (2, 20, 150, 16, 16, 7, 7, 3), (1, 12, 133, 16, 12, 7, 7, 0)]
+                 (2, 20, 150, 16, 16, 7, 7, 3), (1, 12, 133, 16, 12, 7, 7, 0),
+                 # even filter widths; 9x9 in passes of filter rows; 11x11 split over kx (two launches)
+                 (1, 10, 140, 16, 16, 3, 4, 1), (1, 12, 100, 16, 16, 2, 6, 0), (1, 30, 170, 16, 16, 9, 9, 4),
+                 (2, 26, 131, 16, 16, 11, 11, 5), (1, 15, 90, 32, 20, 11, 11, 0)]
 
 
 @pytest.mark.parametrize("shape", DIRECT_SHAPES)
@@ -106,15 +109,16 @@ def test_conv_paper_shape_sampled_pixels(path):
 
 
 # The paper's larger specialised filters ("3x3, 5x5, 7x7, 9x9
-# and 11x11"), 'same' padding, on the default path (R*C > 128 takes the
-# implicit-GEMM kernel) and on SIMT; integer inputs bit-exact.
+# and 11x11"), 'same' padding, on the default path (the direct kernel: 9x9 in
+# passes, 11x11 in two launches over the filter columns), on the implicit-GEMM
+# kernel (TM_CONV_PATH=im2col) and on SIMT; integer inputs bit-exact.
 BIG_FILTERS = [(2, 40, 140, 16, 16, 9, 9, 4), (1, 36, 150, 16, 16, 11, 11, 5), (1, 30, 133, 32, 24, 11, 11, 5)]
 
 
-@pytest.mark.parametrize("algo", [AUTO, SIMT])
+@pytest.mark.parametrize("algo,path", [(AUTO, None), (AUTO, "im2col"), (SIMT, None)])
 @pytest.mark.parametrize("shape", BIG_FILTERS)
-def test_conv_9x9_11x11_filters(algo, shape):
-    X, Wt, Y0, Y = _run(shape, algo)
+def test_conv_9x9_11x11_filters(algo, path, shape):
+    X, Wt, Y0, Y = _run(shape, algo, path=path)
     R, D = oracle.conv2d_nhwc(1.5, X, Wt, 0.5, Y0, shape[-1])
     assert float(np.max(oracle.normalized_error(Y, R, D))) <= TOL
 
