@@ -1,6 +1,8 @@
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck):
 every path on partial tiles, transposes, stream-K, beta = 0 and alpha = 0,
-and the three convolution kernels."""
+the precision variants, the small-GEMM kernel, the three convolution kernels
+(direct incl. passes of filter rows and the two-launch filter split), the blur
+and the loopback distributed schedules (chunked, fused, SUMMA, blur)."""
 import os, sys
 import numpy as np
 import torch
@@ -45,5 +47,42 @@ for (nb, h, w, c, f, r, s, pad) in [(2, 5, 140, 16, 16, 3, 3, 1), (1, 4, 130, 32
             os.environ.pop("TM_CONV_PATH", None)
     Y = torch.rand((nb, ho, wo, f), generator=g, device="cuda")
     tm.conv2d_nhwc(X, Wt, Y, 1.5, 0.5, pad, algo=2)
+# round 2: precision variants, small-GEMM kernel, wide filters, blur, loopback schedules
+for algo in (3, 4):
+    A, B, C = t(300, 200, 200), t(200, 260, 260), t(300, 260, 260)
+    tm.sgemm_ex(A, B, C, 1.5, 0.5, algo)
+A, B, C = t(50, 60), t(60, 70), t(50, 70)
+tm.sgemm_ex(A, B, C, 1.5, 0.5, 0)  # small-GEMM kernel
+for (nb, h, w, c, f, r, s, pad) in [(1, 12, 60, 16, 16, 7, 7, 3), (1, 14, 50, 16, 16, 9, 9, 4),
+                                     (1, 15, 40, 16, 16, 11, 11, 5)]:
+    ho, wo = h + 2 * pad - r + 1, w + 2 * pad - s + 1
+    X, Wt = torch.rand((nb, h, w, c), generator=g, device="cuda"), torch.rand((f, r, s, c), generator=g, device="cuda")
+    Y = torch.rand((nb, ho, wo, f), generator=g, device="cuda")
+    tm.conv2d_nhwc(X, Wt, Y, 1.5, 0.5, pad)
+for (N, M) in [(3, 3), (37, 41), (130, 301)]:
+    img = torch.rand((N, M, 3), generator=g, device="cuda")
+    tm.blur(img)
+    if M > 3:
+        tm.blur(img[:, 1:, :])  # padded pitch, offset base
+P, N, M = 3, 40, 33
+lins, louts = [], []
+for r in range(P):
+    rows = tm.dist_rows(N - 2, P, r)[1]
+    lins.append(torch.rand((rows + 2, M, 3), generator=g, device="cuda"))
+    louts.append(torch.empty((rows, M - 2, 3), device="cuda"))
+tm.blur_dist_loopback(N, M, lins, louts)
+m, n, k = 300, 260, 1100
+A, B = t(m, k), t(k, n)
+for fused in (False, True):
+    As = [A[r0:r0 + rows] for r0, rows in (tm.dist_rows(m, 3, r) for r in range(3))]
+    Cs = [t(rows, n) for _, rows in (tm.dist_rows(m, 3, r) for r in range(3))]
+    Bs = [B.contiguous()] + [torch.empty((k, n), device="cuda") for _ in range(2)]
+    tm.sgemm_dist_loopback(m, n, k, As, Bs, [c.contiguous() for c in Cs], 1.5, 0.5, fused=fused)
+pr, pc = 2, 2
+As, Bs, Cs = [], [], []
+for r in range(pr * pc):
+    (r0, rows), (c0, cols), (a0, ka), (b0, kb) = tm.summa_blocks(m, n, k, pr, pc, r)
+    As.append(t(rows, ka).contiguous()); Bs.append(t(kb, cols).contiguous()); Cs.append(t(rows, cols).contiguous())
+tm.sgemm_summa_loopback(pr, pc, m, n, k, As, Bs, Cs, 1.5, 0.5)
 torch.cuda.synchronize()
 print("sanitize cases done")
