@@ -58,7 +58,11 @@ constexpr int kEpiWarps = 8;
 constexpr int kProducers = 3;      // TMA-issuing warps (0, 2, 3)
 constexpr int kEpiStride = 20;     // floats per staged row (16 data + 4 pad: 16-B aligned, few bank conflicts)
 constexpr int kKcBlocksDefault = 4;   // K_c = 4 * 32 = 128: RZ partial length before RN promotion
-constexpr int kGroupMDefault = 16;    // raster: tile-rows per group (L2 reuse)
+// Raster: tile-rows per group (L2 reuse).  A wave of 74 concurrent 256x256
+// tiles touches GROUP_M A panels and 74/GROUP_M B panels, minimal near
+// sqrt(74): 8 cuts C5's DRAM reads 22.0 -> 18.8 GB per launch at the same
+// throughput as 16 (scripts/r02/groupm.sh).
+constexpr int kGroupMDefault = 8;
 
 // Precision variants of the tensor-core path (template parameter PREC):
 //   kPrecTf32x1  one kind::tf32 MMA per K step on the raw operands (fast, ~2e-3);

@@ -172,3 +172,40 @@ def test_blur_dist_rejects_too_many_ranks():
     louts = [torch.zeros((tm.dist_rows(N - 2, P, r)[1], M - 2, 3), device="cuda") for r in range(P)]
     with pytest.raises(tm.TmError):
         tm.blur_dist_loopback(N, M, lins, louts)
+
+
+@pytest.mark.parametrize("N,M", [(3, 3), (3, 200), (200, 3), (4, 5)])
+def test_blur_minimal_images(N, M):
+    """The smallest images of the iteration domain i < N-2, j < M-2:
+    a single output row, a single output column, a 2x3 output."""
+    import torch
+    import paper_1804_10694_b200 as tm
+    img = si.image(N, M, seed=N + 17 * M, signed=True)
+    R, D = oracle.blur(img)
+    out = tm.blur(torch.from_numpy(img).cuda())
+    torch.cuda.synchronize()
+    assert out.shape == (N - 2, M - 2, 3)
+    assert _err(out.cpu().numpy(), R, D) <= TOL
+
+
+def test_blur_dist_loopback_maximum_ranks():
+    """(N-2)/P == 2: every chunk is exactly the two border rows its upper
+    neighbour needs (the tightest distribution the schedule accepts)."""
+    import torch
+    import paper_1804_10694_b200 as tm
+    P, N, M = 6, 14, 50
+    img = si.image(N, M, seed=99)
+    R, D = oracle.blur(img)
+    lins, louts = [], []
+    for r in range(P):
+        r0, rows = tm.dist_rows(N - 2, P, r)
+        assert rows == 2
+        lin = torch.from_numpy(np.ascontiguousarray(img[r0:r0 + rows + 2])).cuda()
+        if r < P - 1:
+            lin[rows:] = float("nan")
+        lins.append(lin)
+        louts.append(torch.empty((rows, M - 2, 3), device="cuda"))
+    tm.blur_dist_loopback(N, M, lins, louts)
+    torch.cuda.synchronize()
+    got = torch.cat(louts).cpu().numpy()
+    assert _err(got, R, D) <= TOL
