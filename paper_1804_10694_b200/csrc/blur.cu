@@ -149,9 +149,18 @@ tm_status launch_blur(int64_t i0, int64_t i1, int64_t M, const float* in, int64_
   const int64_t Q = 3 * (M - 2);
   if (nrows <= 0 || Q <= 0) return TM_OK;
   const int64_t gx = (Q + kBlurQ - 1) / kBlurQ;
-  const int64_t gy = (nrows + kBlurRows * kBlurWarps - 1) / (kBlurRows * kBlurWarps);
   (void)num_sms;
-  if (gx > 0x7fffffff || gy > 65535) return TM_ERR_INVALID_VALUE;
+  if (gx > 0x7fffffff) return TM_ERR_INVALID_VALUE;
+  // grid.y is limited to 65535 bands of 32 rows: taller images take several launches
+  constexpr int64_t kMaxRows = 65535LL * kBlurRows * kBlurWarps;
+  if (nrows > kMaxRows) {
+    for (int64_t r = 0; r < nrows; r += kMaxRows) {
+      tm_status st = launch_blur(i0 + r, i0 + std::min(nrows, r + kMaxRows), M, in, ldi, out, ldo, num_sms, stream);
+      if (st != TM_OK) return st;
+    }
+    return TM_OK;
+  }
+  const int64_t gy = (nrows + kBlurRows * kBlurWarps - 1) / (kBlurRows * kBlurWarps);
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
   auto al = [](const void* p, unsigned a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
   const bool vin = al(in, 16) && ldi % 4 == 0;

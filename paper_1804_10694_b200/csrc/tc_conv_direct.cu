@@ -343,8 +343,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (valid > 0 && f0 < p.f)
-          epi_store<16>(p.Y, p.f, row0 + valid, p.f, row0, f0, acc, p.alpha, p.beta, stage, lane);
+        // Output pixel row0 + lane owns Y[.., f0 .. f0 + 15]: 16 contiguous
+        // floats (NHWC), so each lane stores its own float4s -- a warp's 30
+        // pixels are one contiguous run of Y, completed in L2 by the four
+        // stores -- with no shared-memory transpose (the GEMM epilogue's
+        // staging cost bank conflicts here).  F % 4 == 0 (tensor-core rule).
+        if (lane < valid && f0 < p.f) {
+          float* yp = p.Y + static_cast<long long>(row0 + lane) * p.f + f0;
+          const int nf = min(16, p.f - f0);
+          float4 cv[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            cv[v] = (p.beta != 0.0f && 4 * v < nf) ? *reinterpret_cast<const float4*>(yp + 4 * v)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            if (4 * v >= nf) continue;
+            float4 o;
+            if (p.beta == 0.0f) {
+              o = make_float4(p.alpha * acc[4 * v], p.alpha * acc[4 * v + 1], p.alpha * acc[4 * v + 2],
+                              p.alpha * acc[4 * v + 3]);
+            } else {
+              o = make_float4(fmaf(p.alpha, acc[4 * v], p.beta * cv[v].x), fmaf(p.alpha, acc[4 * v + 1], p.beta * cv[v].y),
+                              fmaf(p.alpha, acc[4 * v + 2], p.beta * cv[v].z), fmaf(p.alpha, acc[4 * v + 3], p.beta * cv[v].w));
+            }
+            *reinterpret_cast<float4*>(yp + 4 * v) = o;
+          }
+        }
+        (void)stage;
       }
       pph ^= 1;
     }
