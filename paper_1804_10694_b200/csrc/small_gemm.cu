@@ -9,8 +9,10 @@
 // does only that: one CTA of 256 threads per TM x TN output tile (enough tiles
 // to spread over the SMs), beta*C loaded into registers before the main loop
 // so its latency hides behind the operand loads, operands staged through
-// shared memory in BK = 32 slices with the next slice's global loads in flight
-// while the current one is multiplied, and a predicated epilogue (full/partial
+// shared memory in BK = 32 slices with the next TWO slices' global loads in
+// flight (registers, double-buffered: at k = 64 both slices leave in the first
+// round trip instead of the second waiting for the first), and a predicated
+// epilogue (full/partial
 // tile separation).  Each output is the fp32 FMA chain over
 // p = 0..k-1 in order (the textbook loop in fp32).
 #include <cuda_runtime.h>
@@ -74,19 +76,33 @@ __global__ void __launch_bounds__(kSmallThreads) k_sgemm_small(SmallParams p) {
     const int idx = e * kSmallThreads + t;
     if (TB) { q = idx % kSmallBK; j = idx / kSmallBK; } else { j = idx % TN; q = idx / TN; }
   };
-  float ra[LA], rb[LB];
-  auto fetch = [&](int k0) {
+  float ra[2][LA], rb[2][LB];
+  auto fetch = [&](int k0, float (&xa)[LA], float (&xb)[LB]) {
 #pragma unroll
     for (int e = 0; e < LA; ++e) {
       int i, q;
       a_coord(e, i, q);
-      ra[e] = (bm + i < p.m && k0 + q < p.k) ? ld_a<TA>(p, bm + i, k0 + q) : 0.0f;
+      xa[e] = (bm + i < p.m && k0 + q < p.k) ? ld_a<TA>(p, bm + i, k0 + q) : 0.0f;
     }
 #pragma unroll
     for (int e = 0; e < LB; ++e) {
       int q, j;
       b_coord(e, q, j);
-      rb[e] = (k0 + q < p.k && bn + j < p.n) ? ld_b<TB>(p, k0 + q, bn + j) : 0.0f;
+      xb[e] = (k0 + q < p.k && bn + j < p.n) ? ld_b<TB>(p, k0 + q, bn + j) : 0.0f;
+    }
+  };
+  auto stage = [&](const float (&xa)[LA], const float (&xb)[LB]) {
+#pragma unroll
+    for (int e = 0; e < LA; ++e) {
+      int i, q;
+      a_coord(e, i, q);
+      As[q][i] = xa[e];
+    }
+#pragma unroll
+    for (int e = 0; e < LB; ++e) {
+      int q, j;
+      b_coord(e, q, j);
+      Bs[q][j] = xb[e];
     }
   };
 
@@ -96,22 +112,17 @@ __global__ void __launch_bounds__(kSmallThreads) k_sgemm_small(SmallParams p) {
 #pragma unroll
     for (int c = 0; c < RN; ++c) acc[r][c] = 0.0f;
 
-  fetch(0);
-  for (int k0 = 0; k0 < p.k; k0 += kSmallBK) {
-#pragma unroll
-    for (int e = 0; e < LA; ++e) {
-      int i, q;
-      a_coord(e, i, q);
-      As[q][i] = ra[e];
-    }
-#pragma unroll
-    for (int e = 0; e < LB; ++e) {
-      int q, j;
-      b_coord(e, q, j);
-      Bs[q][j] = rb[e];
-    }
+  fetch(0, ra[0], rb[0]);
+  if (kSmallBK < p.k) fetch(kSmallBK, ra[1], rb[1]);
+  int buf = 0;
+  for (int k0 = 0; k0 < p.k; k0 += kSmallBK, buf ^= 1) {
+    if (buf == 0) stage(ra[0], rb[0]);
+    else stage(ra[1], rb[1]);
     __syncthreads();
-    if (k0 + kSmallBK < p.k) fetch(k0 + kSmallBK);  // next slice in flight during the FMAs
+    if (k0 + 2 * kSmallBK < p.k) {  // the slice after next, in flight during the FMAs
+      if (buf == 0) fetch(k0 + 2 * kSmallBK, ra[0], rb[0]);
+      else fetch(k0 + 2 * kSmallBK, ra[1], rb[1]);
+    }
     const int kk = p.k - k0 < kSmallBK ? p.k - k0 : kSmallBK;
     for (int q = 0; q < kk; ++q) {
       float a[RM], b[RN];
