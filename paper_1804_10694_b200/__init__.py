@@ -23,6 +23,8 @@ ALGO_AUTO, ALGO_TF32X3, ALGO_SIMT_F32, ALGO_TF32X1, ALGO_BF16X9 = 0, 1, 2, 3, 4
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_PKG, "_lib", "libtm.so")
+# Tests only (tests/test_product_mutants.py): load a mutant build instead.
+lib_path = os.environ.get("TM_LIB_PATH", lib_path)
 
 # Every function include/tm.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = [

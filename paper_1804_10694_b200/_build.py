@@ -60,13 +60,17 @@ def _compile(src: str, extra: list[str], obj_dir: str) -> tuple[str, list[str]]:
     return obj, cmd
 
 
-def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> str:
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None, out: str | None = None) -> str:
     """Compile every source into a fresh object directory and link libtm.so,
     unless the library's stamp records a build from exactly these sources and
-    flags (force=True always rebuilds).  The stamp lists the nvcc commands."""
+    flags (force=True always rebuilds).  The stamp lists the nvcc commands.
+    out: another library path (tests' mutant builds, e.g. -DTM_MUTATE=1);
+    such builds never replace the product library."""
     extra = list(extra or [])
     if verbose:
         extra += ["-Xptxas", "-v"]
+    if out is not None:
+        return _build_to(out, extra)
     if not force and not _stale(extra):
         return LIB
     import tempfile
@@ -86,6 +90,19 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
         with open(STAMP, "w") as f:
             json.dump(stamp, f, indent=1)
     return LIB
+
+
+def _build_to(out: str, extra: list[str]) -> str:
+    import tempfile
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    with tempfile.TemporaryDirectory(prefix="tm_build_") as obj_dir:
+        with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+            objs = [o for o, _ in ex.map(lambda s: _compile(s, extra, obj_dir), SOURCES)]
+        link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", out, "-ldl"]
+        r = subprocess.run(link, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return out
 
 
 if __name__ == "__main__":

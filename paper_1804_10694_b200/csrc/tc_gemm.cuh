@@ -48,6 +48,18 @@
 #include "ptx.cuh"
 #include "tm_internal.h"
 
+// Mutation testing of the tests (tests/test_product_mutants.py): a library
+// built with -DTM_MUTATE=n breaks exactly one guard on purpose and the named
+// test must then fail ("Mutation tests").  The shipped
+// build has TM_MUTATE == 0 and every TM_MUT(n) is the constant false.
+//   1  the epilogue's partial-tile predicate is ignored (every 4-column group
+//      is stored as a full vector): the guard-band test must fail
+//   2  the B_lo split term is dropped (stored as zero): the 1e-5 parity tests must fail
+#ifndef TM_MUTATE
+#define TM_MUTATE 0
+#endif
+#define TM_MUT(n) (TM_MUTATE == (n))
+
 namespace tmk {
 
 constexpr int kBK = 32;            // K elements per stage (= one 128-byte swizzle row)
@@ -171,6 +183,11 @@ __device__ __forceinline__ uint4 tf32_lo4(uint4 v) {
 
 // Split one smem tile of BYTES (raw -> lo, same offsets, so the same swizzled
 // layout) with 128 threads, 8 loads in flight per thread.
+template <int BYTES>
+__device__ __forceinline__ void zero_tile(uint32_t dst, int st) {  // TM_MUTATE == 2 only
+  for (int idx = st; idx < BYTES / 16; idx += kSplitThreads) ptx::sts128(dst + idx * 16, make_uint4(0u, 0u, 0u, 0u));
+}
+
 template <int BYTES>
 __device__ __forceinline__ void split_tile(uint32_t src, uint32_t dst, int st) {
   constexpr int kChunks = BYTES / 16;
@@ -354,7 +371,7 @@ __device__ __forceinline__ void epi_store_lowreg(float* __restrict__ C, long lon
     __syncwarp();
     const int cc = (lane % G) * 4;
     const int col = col0 + c + cc;
-    const bool full_cols = col + 3 < n;
+    const bool full_cols = TM_MUT(1) || col + 3 < n;
 #pragma unroll
     for (int i0 = 0; i0 < NI; i0 += 2) {  // two row groups per round: 2 C loads in flight, low register use
       float4 v[2], cv[2];
@@ -428,7 +445,7 @@ __device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, 
 #pragma unroll
       for (int sb = 0; sb < SB; ++sb) {
         const int col = col0 + (c0 + sb) * SWD + cc;
-        const bool full_cols = col + 3 < n;
+        const bool full_cols = TM_MUT(1) || col + 3 < n;
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
           cv[sb][i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -456,7 +473,7 @@ __device__ __forceinline__ void epi_store(float* __restrict__ C, long long ldc, 
           __syncwarp();
         }
         const int col = col0 + c + cc;
-        const bool full_cols = col + 3 < n;
+        const bool full_cols = TM_MUT(1) || col + 3 < n;
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
           const int r = (i0 + i) * RPI + lane / G;
@@ -797,7 +814,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             split_tile<Cfg::kABytes>(rawA_s + s * Cfg::kABytes, loA_s + sl * Cfg::kABytes, st);
           }
-          split_tile<Cfg::kBBytes>(rawB_s + s * Cfg::kBBytes, loB_s + sl * Cfg::kBBytes, st);
+          if constexpr (!TM_MUT(2)) split_tile<Cfg::kBBytes>(rawB_s + s * Cfg::kBBytes, loB_s + sl * Cfg::kBBytes, st);
+          else zero_tile<Cfg::kBBytes>(loB_s + sl * Cfg::kBBytes, st);  // mutant: B_lo = 0
           ptx::fence_proxy_async_smem();
         } else if constexpr (BF16) {
           // thread st splits row st of A (128 rows) and, if st < BN_CTA, row st of
