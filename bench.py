@@ -263,12 +263,48 @@ def parity_sample(tm, torch, A, B, C0, alpha, beta, algo, path):
             "pass": err <= tol}
 
 
+def run_reference_blur(args):
+    """--impl reference --config BLUR: the blur oracle on a bounded row sample per
+    step of the paper's 2112x3520 image; GB/s of the algorithmic bytes, scaled."""
+    import numpy as np
+    import oracle
+    import seeded_inputs as si
+    N, M = si.BLUR_IMAGE
+    img = si.image(N, M)
+    vals = []
+    rows = np.arange(0, N - 2, 8, dtype=np.int64)  # every 8th output row: ~264 rows
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.blur(img, rows=rows)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            vals.append(12 * len(rows) * (2 * M - 2) / dt / 1e9)
+    value = statistics.median(vals)
+    full = 12 * (N * M + (N - 2) * (M - 2))
+    line = {"impl": "reference", "metric": "blur GB/s (PAPER.md:216-219 Blur on the 2112x3520 RGB image of PAPER.md:842)",
+            "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(full / (value * 1e9) * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[0,1) RGB image, numpy PCG64)",
+            "config": {"workload": f"blur {N}x{M}x3 (PAPER.md:842)"},
+            "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": oracle.get_threads(), "kind": "oracle",
+                             "sample": f"{len(rows)} of {N - 2} output rows per step; ms_per_step extrapolated"},
+            "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on the host cores, bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import seeded_inputs as si
+    if args.config == "BLUR":
+        return run_reference_blur(args)
+    if args.config == "CONV":
+        print(json.dumps({"impl": "reference", "unavailable": "the CONV line is a SURVEY 8(f) extension; its oracle "
+                                                              "parity runs in tests/test_conv.py (no reference arm)"}))
+        return 0
     m, n, k, desc = workload(args.config)
     budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
     vals = []
