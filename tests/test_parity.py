@@ -259,3 +259,22 @@ def test_auto_offsets_and_views():
         torch.cuda.synchronize()
         An, Bn = Av.cpu().numpy(), Bv.cpu().numpy()
         assert max_err(Cv.cpu().numpy(), An, Bn, Cref, si.ALPHA, si.BETA) <= TOL, off
+
+
+@pytest.mark.parametrize("algo", [AUTO, TF32X3, 4])  # 4 = BF16X9
+def test_random_shape_sweep_sampled_rows(algo):
+    """random shapes up to 2048 (log-uniform m, n, k, 60
+    draws) through AUTO (every dispatch path: small-GEMM, SIMT, tensor cores,
+    stream-K, data-parallel) and forced tensor-core paths; oracle on sampled rows
+    (both ends, every 128-row boundary near the tail, seeded random rows)."""
+    g = si.rng(2048 + algo)
+    for _ in range(60):
+        m, n, k = (int(np.exp(g.uniform(0, np.log(2048)))) for _ in range(3))
+        pad = lambda x: (x + 3) // 4 * 4
+        lda, ldb, ldc = pad(k), pad(n), pad(n)  # aligned, so the forced tensor-core paths accept them
+        A, B, C0 = si.matrices(m, n, k, seed=m * 7919 + n * 31 + k, lda=lda, ldb=ldb, ldc=ldc)
+        C, _ = run(A, B, C0, si.ALPHA, si.BETA, algo, lda=lda, ldb=ldb, ldc=ldc)
+        rows = np.unique(np.concatenate([[0, m - 1], np.arange(max(0, (m // 128) * 128 - 1), m),
+                                         g.integers(0, m, 12)]))[:64].astype(np.int64)
+        e = max_err(C, A, B, C0, si.ALPHA, si.BETA, rows=rows)
+        assert e <= TOL, (m, n, k, e)
