@@ -554,6 +554,7 @@ def run_conv(args):
     paper_default = R == 3 and not args.conv_valid
     traffic, traffic_src = (ncu_traffic("CONV", "tf32x3", 1) if (beta == 0.0 and algo != 2 and paper_default)
                             else (None, None))
+    plan = tm.conv2d_plan_name(Nb, H, W, C, F, R, S, pad, alpha, algo, X.data_ptr(), Wt.data_ptr(), Y.data_ptr())
     # Dominant bound: HBM (X, W, Y once) for the 3x3 / 5x5 shapes, the tensor
     # cores for the large filters (K = R*S*C grows with the filter, the bytes do not)
     _, tpeak, _, tnote = roofline_peak("tf32x3" if algo != 2 else "simt", peaks)
@@ -576,11 +577,10 @@ def run_conv(args):
                          "hbm_frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
                          "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
                          "algorithmic_bytes": algo_bytes,
-                         "kernel": {"direct": "k_conv_direct", "implicit_gemm": "k_sgemm_tc<CONV> (implicit GEMM)",
-                                    "simt": "k_conv_simt"}.get(
-                             tm.conv2d_plan_name(Nb, H, W, C, F, R, S, pad, alpha, algo, X.data_ptr(), Wt.data_ptr(),
-                                                 Y.data_ptr()), "?")},
-            "gpu_launches": args.steps,
+                         "kernel": {"direct": "k_conv_direct", "direct_split": "k_conv_direct (2 launches)",
+                                    "implicit_gemm": "k_sgemm_tc<CONV> (implicit GEMM)", "simt": "k_conv_simt"}.get(
+                             plan, "?")},
+            "gpu_launches": args.steps * (2 if plan == "direct_split" else 1),
             "clocks": clocks.summary()}
     print(json.dumps(line), flush=True)
     return 0

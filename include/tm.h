@@ -172,7 +172,8 @@ tm_status tm_conv2d_nhwc(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f,
                          void* stream, int algo);
 
 /* Name of the kernel tm_conv2d_nhwc would run for these arguments ("direct",
- * "implicit_gemm", "simt", "scale", "noop" or "invalid"); host-only, no
+ * "direct_split" -- the direct kernel in two launches over the filter
+ * columns -- "implicit_gemm", "simt", "scale", "noop" or "invalid"); host-only, no
  * launch (pointers are only inspected for alignment). */
 const char* tm_conv2d_plan_name(int64_t nb, int64_t h, int64_t w, int64_t c, int64_t f, int64_t r, int64_t s,
                                 int64_t pad, float alpha, const float* X, const float* Wt, const float* Y, int algo);

@@ -364,7 +364,8 @@ const char* tm_conv2d_plan_name(int64_t nb, int64_t h, int64_t w, int64_t c, int
                      s <= 128;
   if (algo == TM_ALGO_TF32X3 && !tc_ok) return "invalid";
   if (algo == TM_ALGO_SIMT_F32 || !tc_ok) return "simt";
-  return tmk::conv_direct_fits(a) ? "direct" : "implicit_gemm";
+  const int launches = tmk::conv_direct_launches(a);
+  return launches == 2 ? "direct_split" : launches == 1 ? "direct" : "implicit_gemm";
 }
 
 // Implicit-GEMM convolution.

@@ -523,11 +523,14 @@ static bool dc_split(const ConvArgs& a, DcParams& p1, int& s1, DcParams& p2, int
   return smem1 > 0 && smem2 > 0;
 }
 
-bool conv_direct_fits(const ConvArgs& a) {
+int conv_direct_launches(const ConvArgs& a) {
   DcParams p1, p2;
   int s1, s2, m1, m2;
-  return dc_split(a, p1, s1, p2, s2, m1, m2);
+  if (!dc_split(a, p1, s1, p2, s2, m1, m2)) return 0;
+  return s2 > 0 ? 2 : 1;
 }
+
+bool conv_direct_fits(const ConvArgs& a) { return conv_direct_launches(a) > 0; }
 
 static tm_status launch_taps(const ConvArgs& a, const DcParams& p, int taps, int smem, int num_sms, cudaStream_t stream) {
   switch (taps) {

@@ -111,6 +111,9 @@ tm_status launch_conv_simt(const ConvArgs& a, cudaStream_t stream);
 // Direct (halo-tile) tensor-core convolution for C % 16 == 0, F <= 64 and
 // filters that fit in shared memory (tc_conv_direct.cu).
 bool conv_direct_fits(const ConvArgs& a);
+// Launches the direct kernel takes for this shape: 1, 2 (filter columns split
+// over two launches), or 0 (does not fit).
+int conv_direct_launches(const ConvArgs& a);
 tm_status launch_conv_direct(const ConvArgs& a, int num_sms, cudaStream_t stream);
 
 // Measured-configuration cache (tune.cpp): the tuned choice for this problem

@@ -200,7 +200,7 @@ def test_conv_plan_names_for_the_paper_filter_sizes():
     filter columns); 25x25 does not fit a warp's shift -> implicit GEMM;
     channels not a multiple of 16 -> SIMT; host-only."""
     assert tm.conv2d_plan_name(1, 64, 64, 16, 16, 25, 25, 12) == "implicit_gemm"
-    for r, want in ((1, "direct"), (3, "direct"), (5, "direct"), (7, "direct"), (9, "direct"), (11, "direct")):
+    for r, want in ((1, "direct"), (3, "direct"), (5, "direct"), (7, "direct"), (9, "direct"), (11, "direct_split")):
         assert tm.conv2d_plan_name(32, 512, 512, 16, 16, r, r, r // 2) == want, r
     assert tm.conv2d_plan_name(1, 8, 8, 18, 16, 3, 3, 1) == "simt"
     assert tm.conv2d_plan_name(1, 8, 8, 16, 16, 3, 3, 1, alpha=0.0) == "scale"
