@@ -39,6 +39,8 @@
 //                  full / partial tile separation).  The epilogue is the
 //                  longest per-tile chain, hence two groups.
 #include <algorithm>
+#include <cstdio>
+#include <vector>
 
 #include "tc_gemm.cuh"
 
@@ -65,7 +67,13 @@ struct DcParams {
   int kx0;             // first filter column kx of this launch (kx split: 0, then S of the first)
   int tiles_x, num_tiles;
   int chunks;          // c / 16
-  int stages;          // r * chunks: K = 16 * stages (resident filter stages)
+  int stages;          // rin * chunks: K = 16 * stages (resident filter stages)
+  int ro;              // output rows per tile (1, or 2 when the MMA N of one row is small)
+  int rin;             // input rows per tile: r + ro - 1
+  int ho_t;            // tile rows per image: ceil(ho / ro)
+  int nrow;            // MMA N of one output row: fp * S
+  int fstages;         // raw filter boxes r * chunks (ro == 2: staged, then expanded)
+  int fbox;            // one raw filter box: nrow rows x 64 B
   int rpp, passes;     // filter rows per pass, passes per tile (last may be shorter)
   int pstages;         // stages of a full pass: rpp * chunks <= kDcMaxStages
   int cw;              // channels per halo box (16 or 32)
@@ -80,17 +88,33 @@ struct DcParams {
   uint32_t idesc;
   float alpha, beta;
   float* Y;
+  unsigned long long* stats;  // debug (TM_CONV_STATS): [grid][16] cycles per role and wait, or null
 };
 
+// Role timing for TM_CONV_STATS (null stats: no cost beyond the branch).
+enum DcStat { kStMmaWaitAcc, kStMmaWaitReady, kStMmaTotal, kStSplitWaitHalo, kStSplitWaitSlot, kStSplitTotal,
+              kStEpiWaitAcc, kStEpiTotal, kStProdWaitSlot, kStProdTotal };
+#define DC_TIMED(slot, stmt)                                      \
+  do {                                                            \
+    if constexpr (ST) {                                           \
+      const long long t0_ = clock64();                            \
+      stmt;                                                       \
+      st_acc[slot] += static_cast<unsigned long long>(clock64() - t0_); \
+    } else {                                                      \
+      stmt;                                                       \
+    }                                                             \
+  } while (0)
+
+// Tile t -> image b, first output row y (ro rows per tile), first output column x0.
 __device__ __forceinline__ void dc_tile(const DcParams& p, int t, int& b, int& y, int& x0) {
   const int xt = t % p.tiles_x;
   const int rest = t / p.tiles_x;
-  y = rest % p.ho;
-  b = rest / p.ho;
+  y = (rest % p.ho_t) * p.ro;
+  b = rest / p.ho_t;
   x0 = xt * 4 * p.ow;
 }
 
-template <int S>
+template <int S, bool ST = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_direct(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, DcParams p) {
   extern __shared__ uint8_t smem_raw_[];
@@ -98,8 +122,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* bres = smem;
   uint8_t* bres_lo = bres + p.bres_bytes;
   uint8_t* halo = bres_lo + p.bres_bytes;
-  float* epi_stage = reinterpret_cast<float*>(halo + p.n_slots * p.slot_bytes);
-  uint64_t* bres_full = reinterpret_cast<uint64_t*>(epi_stage + kDcEpiWarps * 32 * kEpiStride);
+  uint8_t* fstage = halo + p.n_slots * p.slot_bytes;  // ro == 2: raw filter boxes before expansion
+  uint64_t* bres_full = reinterpret_cast<uint64_t*>(fstage + (p.ro == 2 ? p.fstages * p.fbox : 0));
   uint64_t* halo_full = bres_full + 1;            // [n_slots] TMA landed
   uint64_t* halo_empty = halo_full + p.n_slots;   // [n_slots] split warps done reading
   uint64_t* ready = halo_empty + p.n_slots;       // [kDcMaxSlots] A slot written
@@ -110,6 +134,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  unsigned long long st_acc[ST ? 16 : 1] = {};
+  const long long st_t0 = ST ? clock64() : 0;
+  (void)st_acc;
+  (void)st_t0;
   if (threadIdx.x == 0) {
     ptx::mbar_init(bres_full, 1);
     for (int i = 0; i < p.n_slots; ++i) {
@@ -146,10 +174,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (pi == 0) {
           // filters: stage (ky, ci) = box {16 channels, S taps, 1, fp filters}
           // -> rows (f, kx) x 64 B, i.e. B^T of the Z GEMM for this K block
-          ptx::mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.stages * p.bbox));
-          for (int s = 0; s < p.stages; ++s) {
+          // (ro == 2: into the staging area; the split warps expand them)
+          uint8_t* fdst = p.ro == 2 ? fstage : bres;
+          ptx::mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.fstages * p.fbox));
+          for (int s = 0; s < p.fstages; ++s) {
             const int ky = s / p.chunks, ci = s - ky * p.chunks;
-            ptx::tma_load_4d(bres + s * p.bbox, &tmW, bres_full, ci * kDcBK, 0, p.kx0, ky);
+            ptx::tma_load_4d(fdst + s * p.fbox, &tmW, bres_full, ci * kDcBK, 0, p.kx0, ky);
           }
         }
         int slot = 0, own = 0;
@@ -160,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (own == pi) {
             int b, y, x0;
             dc_tile(p, t, b, y, x0);
-            ptx::mbar_wait(&halo_empty[slot], ph ^ 1);
+            DC_TIMED(kStProdWaitSlot, ptx::mbar_wait(&halo_empty[slot], ph ^ 1));
             ptx::mbar_arrive_expect_tx(&halo_full[slot], static_cast<uint32_t>(boxes * p.rpp * p.halo_w * p.cw * 4));
             for (int i = 0; i < boxes; ++i)
               ptx::tma_load_4d(halo + slot * p.slot_bytes + i * p.box_bytes, &tmX, &halo_full[slot], i * p.cw,
@@ -170,8 +200,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               // contiguous run of the output row): stage it in L2 now, the
               // halo ring depth ahead of its use
               const int cnt = min(4 * p.ow, p.wo - x0);
-              ptx::prefetch_l2_bulk(p.Y + static_cast<long long>((b * p.ho + y) * p.wo + x0) * p.f,
-                                    static_cast<uint32_t>(cnt * p.f * 4));
+              for (int o = 0; o < p.ro && y + o < p.ho; ++o)
+                ptx::prefetch_l2_bulk(p.Y + static_cast<long long>((b * p.ho + y + o) * p.wo + x0) * p.f,
+                                      static_cast<uint32_t>(cnt * p.f * 4));
             }
           }
           if (++own == kDcProducers) own = 0;
@@ -188,12 +219,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int sl = 0, pb = 0;
       uint32_t phl = 0, pph = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        ptx::mbar_wait(&part_empty[pb], pph ^ 1);
+        DC_TIMED(kStMmaWaitAcc, ptx::mbar_wait(&part_empty[pb], pph ^ 1));
         const uint32_t d = tmem_base + static_cast<uint32_t>(pb * p.n);
         uint32_t boff = 0;
         int sg = 0;  // filter stage (global over the passes)
         for (int ps = 0; ps < p.passes; ++ps) {
-          ptx::mbar_wait(&ready[sl], phl);
+          DC_TIMED(kStMmaWaitReady, ptx::mbar_wait(&ready[sl], phl));
           ptx::tc_fence_after();
           uint32_t a = tmem_base + acol + static_cast<uint32_t>(sl * p.a_cols);
           const int ns = min(p.pstages, p.stages - sg);
@@ -223,6 +254,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       // resident filters: lo = split of hi, same layout (elementwise)
       const int st = q * 32 + lane;
       ptx::mbar_wait(bres_full, 0);
+      if (p.ro == 2) {
+        // Expand the raw boxes (rows (kx, f) of filter row ky) into the two-row
+        // B^T: stage (input row j, channels ci), row (o, kx, f) = W[f, j - o, kx, c]
+        // when 0 <= j - o < r, else zero.  16-B chunks through the SWIZZLE_64B
+        // pattern of both layouts (chunk c of row r at c ^ ((r / 2) % 4); boxes
+        // 1 KiB aligned).
+        const uint32_t fs = ptx::smem_u32(fstage), bd = ptx::smem_u32(bres);
+        const int per_stage = p.n * 4;  // 16-B chunks per expanded stage
+        for (int i = st; i < p.stages * per_stage; i += 128) {
+          const int sg = i / per_stage, rem = i - sg * per_stage;
+          const int rr = rem >> 2, c = rem & 3;
+          const int j = sg / p.chunks, ci = sg - j * p.chunks;
+          const int o = rr / p.nrow, qrow = rr - o * p.nrow, ky = j - o;
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          if (ky >= 0 && ky < p.r)
+            v = ptx::lds128(fs + (ky * p.chunks + ci) * p.fbox + qrow * 64 + ((c ^ ((qrow >> 1) & 3)) << 4));
+          ptx::sts128(bd + sg * p.bbox + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4), v);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // split warpgroup: expansion done before the lo pass
+      }
       const uint32_t src = ptx::smem_u32(bres), dst = ptx::smem_u32(bres_lo);
       for (int i = st; i < p.bres_bytes / 16; i += 128) ptx::sts128(dst + i * 16, tf32_lo4(ptx::lds128(src + i * 16)));
       ptx::fence_proxy_async_smem();
@@ -253,8 +304,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int ps = 0; ps < p.passes; ++ps) {
       {
         const int ns = min(p.pstages, p.stages - ps * p.pstages);
-        ptx::mbar_wait(&halo_full[slot], ph);
-        ptx::mbar_wait(&a_empty[sl], phl ^ 1);
+        DC_TIMED(kStSplitWaitHalo, ptx::mbar_wait(&halo_full[slot], ph));
+        DC_TIMED(kStSplitWaitSlot, ptx::mbar_wait(&a_empty[sl], phl ^ 1));
         ptx::tc_fence_after();
         const uint32_t hb = halo_s + slot * p.slot_bytes;
         const uint32_t ta = trow + static_cast<uint32_t>(sl * p.a_cols);
@@ -298,21 +349,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::setmaxnreg_inc<152>();
     const int q = warp & 3;
     const int e = (warp - 8) >> 2;
-    float* stage = epi_stage + (warp - 8) * 32 * kEpiStride;
     const int pb = e;
     uint32_t pph = 0;
     int i = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++i) {
       if (i % p.n_part != e) continue;
-      ptx::mbar_wait(&part_full[pb], pph);
+      DC_TIMED(kStEpiWaitAcc, ptx::mbar_wait(&part_full[pb], pph));
       ptx::tc_fence_after();
       int b, y, x0;
       dc_tile(p, t, b, y, x0);
       const int xw = x0 + p.ow * q;                        // first output pixel of this warp
       const int valid = min(p.ow, p.wo - xw);              // outputs of this warp (lanes 0 .. valid-1)
-      const int row0 = (b * p.ho + y) * p.wo + xw;         // its GEMM row (output pixel index)
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(pb * p.n);
+      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(pb * p.n);
+      // ro output rows per tile: row o's Z columns start at o * nrow
+      for (int o = 0; o < p.ro; ++o)
       for (int f0 = 0; f0 < p.fp; f0 += 16) {
+        const int row0 = (b * p.ho + y + o) * p.wo + xw;   // this warp's first GEMM row (output pixel)
+        const bool row_ok = y + o < p.ho;                  // the last tile row of an odd ho has one row
+        const uint32_t taddr = tacc + static_cast<uint32_t>(o * p.nrow);
         // column kx * fp + f holds Z[., (f, kx)]: per kx, 16 consecutive columns
         // of filters f0 .. f0 + 15; loads in groups of KG taps (registers)
         constexpr int KG = S <= 7 ? S : (S + 1) / 2;
@@ -325,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (k0 + c < S)
               ptx::tmem_ld_32x32b_x16(taddr + (k0 + c) * p.fp + f0, *reinterpret_cast<uint32_t(*)[16]>(r + 16 * c));
           ptx::tmem_ld_wait();
-          if (f0 + 16 >= p.fp && k0 + KG >= S) {  // last read of this accumulator: hand it back to the MMA
+          if (o + 1 == p.ro && f0 + 16 >= p.fp && k0 + KG >= S) {  // last read of this accumulator: hand it back
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&part_empty[pb]);
@@ -348,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // pixels are one contiguous run of Y, completed in L2 by the four
         // stores -- with no shared-memory transpose (the GEMM epilogue's
         // staging cost bank conflicts here).  F % 4 == 0 (tensor-core rule).
-        if (lane < valid && f0 < p.f) {
+        if (row_ok && lane < valid && f0 < p.f) {
           float* yp = p.Y + static_cast<long long>(row0 + lane) * p.f + f0;
           const int nf = min(16, p.f - f0);
           float4 cv[4];
@@ -370,12 +424,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<float4*>(yp + 4 * v) = o;
           }
         }
-        (void)stage;
       }
       pph ^= 1;
     }
   }
 
+  if constexpr (ST) {  // one representative thread per role: producer 0, MMA, split warp 4, epilogue warp 8
+    const unsigned long long total = static_cast<unsigned long long>(clock64() - st_t0);
+    unsigned long long* o = p.stats + static_cast<long long>(blockIdx.x) * 16;
+    if (threadIdx.x == 0) { o[kStProdWaitSlot] = st_acc[kStProdWaitSlot]; o[kStProdTotal] = total; }
+    if (warp == 1 && lane == 0) { o[kStMmaWaitAcc] = st_acc[kStMmaWaitAcc]; o[kStMmaWaitReady] = st_acc[kStMmaWaitReady]; o[kStMmaTotal] = total; }
+    if (warp == 4 && lane == 0) { o[kStSplitWaitHalo] = st_acc[kStSplitWaitHalo]; o[kStSplitWaitSlot] = st_acc[kStSplitWaitSlot]; o[kStSplitTotal] = total; }
+    if (warp == 8 && lane == 0) { o[kStEpiWaitAcc] = st_acc[kStEpiWaitAcc]; o[kStEpiTotal] = total; }
+  }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -441,26 +502,39 @@ int dc_plan(const ConvArgs& a, DcParams& p, int kx0, int taps) {
   p.ho = static_cast<int>(ho);
   p.wo = static_cast<int>(wo);
   p.fp = (p.f + 15) / 16 * 16;
-  p.n = p.fp * taps;
-  if (p.n > 256) return 0;
+  if (p.fp * taps > 256) return 0;
   p.ow = 33 - static_cast<int>(a.s);
   p.kx0 = kx0;
   p.tiles_x = static_cast<int>((wo + 4 * p.ow - 1) / (4 * p.ow));
-  const int64_t tiles = a.nb * ho * p.tiles_x;
+  const int64_t tiles = a.nb * ((ho + 1) / 2 * 2) * p.tiles_x;  // bound for either ro (exact count below)
   if (tiles > INT32_MAX / 2 || a.nb * ho * wo > INT32_MAX / 2) return 0;
-  p.num_tiles = static_cast<int>(tiles);
+  (void)tiles;
   p.chunks = p.c / kDcBK;
   if (p.chunks > kDcMaxStages) return 0;
-  p.stages = p.r * p.chunks;
+  // Two output rows per tile when one row's MMA N is small (<= 48: the
+  // kind::tf32 floor of ~45 cycles per MMA leaves N = 96 nearly free): input
+  // rows r + 1 instead of 2r, N doubled, MMA cycles per output row -29 % at
+  // 3x3 x 16 filters; the (j, o) blocks with j - o outside [0, r) are zeros.
+  static const int env_ro = [] { const char* e = std::getenv("TM_CONV_RO"); return e ? std::atoi(e) : 0; }();
+  p.nrow = p.fp * taps;
+  p.ro = (env_ro == 1 || p.r < 2 || 2 * p.nrow > 96) ? 1 : 2;
+  if (env_ro == 2 && 2 * p.nrow <= 256 && p.r >= 2) p.ro = 2;
+  p.rin = p.r + p.ro - 1;
+  p.n = p.ro * p.nrow;
+  p.ho_t = (p.ho + p.ro - 1) / p.ro;
+  p.fstages = p.r * p.chunks;
+  p.fbox = p.nrow * kDcBK * 4;
+  p.stages = p.rin * p.chunks;
   p.cw = p.c % 32 == 0 ? 32 : 16;
   p.halo_w = 3 * p.ow + 32;
+  p.num_tiles = static_cast<int>(a.nb * p.ho_t * p.tiles_x);
   p.bbox = p.n * kDcBK * 4;
   p.bres_bytes = p.stages * p.bbox;
-  const int fixed = 1024 + 2 * p.bres_bytes + kDcEpiWarps * 32 * kEpiStride * 4 + 512;
+  const int fixed = 1024 + 2 * p.bres_bytes + (p.ro == 2 ? p.fstages * p.fbox : 0) + 512;
   if (fixed >= kDcMaxSmem) return 0;
   int best_rpp = 0, best_slots = 0, best_part = 0;
   for (int want_slots = 2; want_slots >= 1 && !best_rpp; --want_slots) {
-    for (int rpp = std::min(p.r, kDcMaxStages / p.chunks); rpp >= 1; --rpp) {
+    for (int rpp = std::min(p.rin, kDcMaxStages / p.chunks); rpp >= 1; --rpp) {
       const int a_cols = rpp * p.chunks * 2 * kDcBK;
       int part = 2, slots = (512 - 2 * p.n) / a_cols;
       if (slots < want_slots) { part = 1; slots = (512 - p.n) / a_cols; }
@@ -475,7 +549,7 @@ int dc_plan(const ConvArgs& a, DcParams& p, int kx0, int taps) {
   }
   if (!best_rpp) return 0;
   p.rpp = best_rpp;
-  p.passes = (p.r + p.rpp - 1) / p.rpp;
+  p.passes = (p.rin + p.rpp - 1) / p.rpp;
   p.pstages = p.rpp * p.chunks;
   p.a_cols = p.pstages * 2 * kDcBK;
   p.n_part = best_part;
@@ -500,8 +574,36 @@ tm_status launch_dc(const ConvArgs& a, const DcParams& p, int smem, int num_sms,
   static std::atomic<unsigned long long> optin{0};  // per instantiation, bit per device
   if (tm_status st = ensure_smem_optin(optin, kern, kDcMaxSmem); st != TM_OK) return st;
   const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
-  kern<<<grid, kThreads, smem, stream>>>(tmX, tmW, p);
-  return cudaPeekAtLastError() == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+  const char* stats_path = std::getenv("TM_CONV_STATS");  // debug: per-role wait breakdown (scripts/r02/)
+  if (!stats_path) {
+    kern<<<grid, kThreads, smem, stream>>>(tmX, tmW, p);
+    return cudaPeekAtLastError() == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+  }
+  DcParams q = p;
+  if (cudaMalloc(&q.stats, sizeof(unsigned long long) * 16 * grid) != cudaSuccess) return TM_ERR_CUDA;
+  cudaMemsetAsync(q.stats, 0, sizeof(unsigned long long) * 16 * grid, stream);
+  auto kst = k_conv_direct<S, true>;
+  static std::atomic<unsigned long long> optin_st{0};
+  if (tm_status st = ensure_smem_optin(optin_st, kst, kDcMaxSmem); st != TM_OK) return st;
+  kst<<<grid, kThreads, smem, stream>>>(tmX, tmW, q);
+  if (cudaPeekAtLastError() != cudaSuccess) return TM_ERR_CUDA;
+  std::vector<unsigned long long> h(16 * grid);
+  cudaStreamSynchronize(stream);
+  cudaMemcpy(h.data(), q.stats, sizeof(unsigned long long) * 16 * grid, cudaMemcpyDeviceToHost);
+  cudaFree(q.stats);
+  if (FILE* f = std::fopen(stats_path, "a")) {
+    static const char* names[] = {"mma_wait_acc", "mma_wait_ready", "mma_total", "split_wait_halo", "split_wait_slot",
+                                  "split_total", "epi_wait_acc", "epi_total", "prod_wait_slot", "prod_total"};
+    std::fprintf(f, "{\"S\": %d, \"tiles\": %d, \"grid\": %d", S, p.num_tiles, grid);
+    for (int k = 0; k < 10; ++k) {
+      double sum = 0;
+      for (int b = 0; b < grid; ++b) sum += static_cast<double>(h[b * 16 + k]);
+      std::fprintf(f, ", \"%s\": %.0f", names[k], sum / grid);
+    }
+    std::fprintf(f, "}\n");
+    std::fclose(f);
+  }
+  return TM_OK;
 }
 
 }  // namespace
