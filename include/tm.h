@@ -409,7 +409,9 @@ tm_status tm_sgemm_summa_loopback(int pr, int pc, int64_t m, int64_t n, int64_t 
  * tm_ce_connect.  Every call passes the all-gathered tm_ipc_export of each
  * rank's B buffer (re-export when a buffer changes).  Device memory must come
  * from cudaMalloc (or torch's default caching allocator); one process per
- * device, or several processes sharing a device (the tests do).
+ * device, or several processes sharing a device (the tests do).  A tm_ce_t
+ * must not be used by two host threads at once; peer mappings it opened stay
+ * mapped until tm_ce_destroy.
  * ------------------------------------------------------------------------- */
 typedef struct { unsigned char bytes[64]; int64_t offset; } tm_ipc_buf; /* IPC handle of the allocation + byte offset */
 typedef struct tm_ce_s* tm_ce_t;
