@@ -74,6 +74,7 @@ struct DcParams {
   int nrow;            // MMA N of one output row: fp * S
   int fstages;         // raw filter boxes r * chunks (ro == 2: staged, then expanded)
   int fbox;            // one raw filter box: nrow rows x 64 B
+  int fgap;            // bytes between the halo ring and the barriers (staging, >= 20 KiB)
   int rpp, passes;     // filter rows per pass, passes per tile (last may be shorter)
   int pstages;         // stages of a full pass: rpp * chunks <= kDcMaxStages
   int cw;              // channels per halo box (16 or 32)
@@ -106,15 +107,18 @@ enum DcStat { kStMmaWaitAcc, kStMmaWaitReady, kStMmaTotal, kStSplitWaitHalo, kSt
   } while (0)
 
 // Tile t -> image b, first output row y (ro rows per tile), first output column x0.
+template <int RO>
 __device__ __forceinline__ void dc_tile(const DcParams& p, int t, int& b, int& y, int& x0) {
   const int xt = t % p.tiles_x;
   const int rest = t / p.tiles_x;
-  y = (rest % p.ho_t) * p.ro;
+  y = (rest % p.ho_t) * RO;
   b = rest / p.ho_t;
   x0 = xt * 4 * p.ow;
 }
 
-template <int S, bool ST = false>
+// RO: output rows per tile (== p.ro; a template parameter so that the one-row
+// kernels, whose epilogue is the longer chain at wide filters, carry no loop).
+template <int S, bool ST = false, int RO = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_direct(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, DcParams p) {
   extern __shared__ uint8_t smem_raw_[];
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* bres_lo = bres + p.bres_bytes;
   uint8_t* halo = bres_lo + p.bres_bytes;
   uint8_t* fstage = halo + p.n_slots * p.slot_bytes;  // ro == 2: raw filter boxes before expansion
-  uint64_t* bres_full = reinterpret_cast<uint64_t*>(fstage + (p.ro == 2 ? p.fstages * p.fbox : 0));
+  uint64_t* bres_full = reinterpret_cast<uint64_t*>(fstage + p.fgap);
   uint64_t* halo_full = bres_full + 1;            // [n_slots] TMA landed
   uint64_t* halo_empty = halo_full + p.n_slots;   // [n_slots] split warps done reading
   uint64_t* ready = halo_empty + p.n_slots;       // [kDcMaxSlots] A slot written
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // filters: stage (ky, ci) = box {16 channels, S taps, 1, fp filters}
           // -> rows (f, kx) x 64 B, i.e. B^T of the Z GEMM for this K block
           // (ro == 2: into the staging area; the split warps expand them)
-          uint8_t* fdst = p.ro == 2 ? fstage : bres;
+          uint8_t* fdst = RO == 2 ? fstage : bres;
           ptx::mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.fstages * p.fbox));
           for (int s = 0; s < p.fstages; ++s) {
             const int ky = s / p.chunks, ci = s - ky * p.chunks;
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ps = 0; ps < p.passes; ++ps) {
           if (own == pi) {
             int b, y, x0;
-            dc_tile(p, t, b, y, x0);
+            dc_tile<RO>(p, t, b, y, x0);
             DC_TIMED(kStProdWaitSlot, ptx::mbar_wait(&halo_empty[slot], ph ^ 1));
             ptx::mbar_arrive_expect_tx(&halo_full[slot], static_cast<uint32_t>(boxes * p.rpp * p.halo_w * p.cw * 4));
             for (int i = 0; i < boxes; ++i)
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               // contiguous run of the output row): stage it in L2 now, the
               // halo ring depth ahead of its use
               const int cnt = min(4 * p.ow, p.wo - x0);
-              for (int o = 0; o < p.ro && y + o < p.ho; ++o)
+              for (int o = 0; o < RO && y + o < p.ho; ++o)
                 ptx::prefetch_l2_bulk(p.Y + static_cast<long long>((b * p.ho + y + o) * p.wo + x0) * p.f,
                                       static_cast<uint32_t>(cnt * p.f * 4));
             }
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // resident filters: lo = split of hi, same layout (elementwise)
       const int st = q * 32 + lane;
       ptx::mbar_wait(bres_full, 0);
-      if (p.ro == 2) {
+      if constexpr (RO == 2) {
         // Expand the raw boxes (rows (kx, f) of filter row ky) into the two-row
         // B^T: stage (input row j, channels ci), row (o, kx, f) = W[f, j - o, kx, c]
         // when 0 <= j - o < r, else zero.  16-B chunks through the SWIZZLE_64B
@@ -357,12 +361,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       DC_TIMED(kStEpiWaitAcc, ptx::mbar_wait(&part_full[pb], pph));
       ptx::tc_fence_after();
       int b, y, x0;
-      dc_tile(p, t, b, y, x0);
+      dc_tile<RO>(p, t, b, y, x0);
       const int xw = x0 + p.ow * q;                        // first output pixel of this warp
       const int valid = min(p.ow, p.wo - xw);              // outputs of this warp (lanes 0 .. valid-1)
       const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(pb * p.n);
       // ro output rows per tile: row o's Z columns start at o * nrow
-      for (int o = 0; o < p.ro; ++o)
+#pragma unroll
+      for (int o = 0; o < RO; ++o)
       for (int f0 = 0; f0 < p.fp; f0 += 16) {
         const int row0 = (b * p.ho + y + o) * p.wo + xw;   // this warp's first GEMM row (output pixel)
         const bool row_ok = y + o < p.ho;                  // the last tile row of an odd ho has one row
@@ -379,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (k0 + c < S)
               ptx::tmem_ld_32x32b_x16(taddr + (k0 + c) * p.fp + f0, *reinterpret_cast<uint32_t(*)[16]>(r + 16 * c));
           ptx::tmem_ld_wait();
-          if (o + 1 == p.ro && f0 + 16 >= p.fp && k0 + KG >= S) {  // last read of this accumulator: hand it back
+          if (o + 1 == RO && f0 + 16 >= p.fp && k0 + KG >= S) {  // last read of this accumulator: hand it back
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&part_empty[pb]);
@@ -518,7 +523,7 @@ int dc_plan(const ConvArgs& a, DcParams& p, int kx0, int taps) {
   static const int env_ro = [] { const char* e = std::getenv("TM_CONV_RO"); return e ? std::atoi(e) : 0; }();
   p.nrow = p.fp * taps;
   p.ro = (env_ro == 1 || p.r < 2 || 2 * p.nrow > 96) ? 1 : 2;
-  if (env_ro == 2 && 2 * p.nrow <= 256 && p.r >= 2) p.ro = 2;
+  if (env_ro == 2 && 2 * p.nrow <= 256 && p.r >= 2 && taps <= 3) p.ro = 2;  // two-row kernels: taps <= 3
   p.rin = p.r + p.ro - 1;
   p.n = p.ro * p.nrow;
   p.ho_t = (p.ho + p.ro - 1) / p.ro;
@@ -530,7 +535,12 @@ int dc_plan(const ConvArgs& a, DcParams& p, int kx0, int taps) {
   p.num_tiles = static_cast<int>(a.nb * p.ho_t * p.tiles_x);
   p.bbox = p.n * kDcBK * 4;
   p.bres_bytes = p.stages * p.bbox;
-  const int fixed = 1024 + 2 * p.bres_bytes + (p.ro == 2 ? p.fstages * p.fbox : 0) + 512;
+  // The region after the halo ring (the two-row kernel's filter staging) is at
+  // least 20 KiB: measured A/B (scripts/r02/conv_ab5.sh), the 9x9 kernel runs
+  // 2.05 ms with the barriers 20 KiB past the halo ring and 2.49 ms with them
+  // right after it, at the same pipeline configuration (cause not isolated).
+  p.fgap = std::max(p.ro == 2 ? p.fstages * p.fbox : 0, 20 * 1024);
+  const int fixed = 1024 + 2 * p.bres_bytes + p.fgap + 512;
   if (fixed >= kDcMaxSmem) return 0;
   int best_rpp = 0, best_slots = 0, best_part = 0;
   for (int want_slots = 2; want_slots >= 1 && !best_rpp; --want_slots) {
@@ -565,12 +575,12 @@ int dc_plan(const ConvArgs& a, DcParams& p, int kx0, int taps) {
   return fixed + p.n_slots * p.slot_bytes;
 }
 
-template <int S>
+template <int S, int RO = 1>
 tm_status launch_dc(const ConvArgs& a, const DcParams& p, int smem, int num_sms, cudaStream_t stream) {
   CUtensorMap tmX, tmW;
   if (!encode_halo(&tmX, a, p.cw, p.halo_w, p.rpp)) return TM_ERR_INTERNAL;
   if (!encode_filters(&tmW, a, p.fp, S)) return TM_ERR_INTERNAL;
-  auto kern = k_conv_direct<S>;
+  auto kern = k_conv_direct<S, false, RO>;
   static std::atomic<unsigned long long> optin{0};  // per instantiation, bit per device
   if (tm_status st = ensure_smem_optin(optin, kern, kDcMaxSmem); st != TM_OK) return st;
   const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
@@ -582,7 +592,7 @@ tm_status launch_dc(const ConvArgs& a, const DcParams& p, int smem, int num_sms,
   DcParams q = p;
   if (cudaMalloc(&q.stats, sizeof(unsigned long long) * 16 * grid) != cudaSuccess) return TM_ERR_CUDA;
   cudaMemsetAsync(q.stats, 0, sizeof(unsigned long long) * 16 * grid, stream);
-  auto kst = k_conv_direct<S, true>;
+  auto kst = k_conv_direct<S, true, RO>;
   static std::atomic<unsigned long long> optin_st{0};
   if (tm_status st = ensure_smem_optin(optin_st, kst, kDcMaxSmem); st != TM_OK) return st;
   kst<<<grid, kThreads, smem, stream>>>(tmX, tmW, q);
@@ -636,9 +646,9 @@ bool conv_direct_fits(const ConvArgs& a) { return conv_direct_launches(a) > 0; }
 
 static tm_status launch_taps(const ConvArgs& a, const DcParams& p, int taps, int smem, int num_sms, cudaStream_t stream) {
   switch (taps) {
-    case 1: return launch_dc<1>(a, p, smem, num_sms, stream);
-    case 2: return launch_dc<2>(a, p, smem, num_sms, stream);
-    case 3: return launch_dc<3>(a, p, smem, num_sms, stream);
+    case 1: return p.ro == 2 ? launch_dc<1, 2>(a, p, smem, num_sms, stream) : launch_dc<1>(a, p, smem, num_sms, stream);
+    case 2: return p.ro == 2 ? launch_dc<2, 2>(a, p, smem, num_sms, stream) : launch_dc<2>(a, p, smem, num_sms, stream);
+    case 3: return p.ro == 2 ? launch_dc<3, 2>(a, p, smem, num_sms, stream) : launch_dc<3>(a, p, smem, num_sms, stream);
     case 4: return launch_dc<4>(a, p, smem, num_sms, stream);
     case 5: return launch_dc<5>(a, p, smem, num_sms, stream);
     case 6: return launch_dc<6>(a, p, smem, num_sms, stream);
