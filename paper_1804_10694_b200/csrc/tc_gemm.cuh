@@ -132,11 +132,17 @@ struct TcParams {
   int tiles_m, tiles_n, num_tiles, kblocks;
   int kc_blocks;  // K-blocks per TMEM partial (K_c / 32)
   int group_m;    // raster group height in tiles
-  // stream-K: the tiles x kblocks iteration space is cut
-  // into equal contiguous ranges, one per cluster; tiles split between clusters
-  // are reduced in a fixed order through a workspace (deterministic).
+  // stream-K: the iteration space of the first
+  // sk_tiles tiles (sk_tiles x kblocks) is cut into equal contiguous ranges, one
+  // per cluster; tiles split between clusters are reduced in a fixed order
+  // through a workspace (deterministic).  Hybrid schedule: sk_tiles < num_tiles
+  // -- every cluster first works its stream-K share, then the remaining tiles
+  // whole, data-parallel (tile sk_tiles + cluster + j * clusters), so the
+  // fixed-order reductions overlap whole tiles' streaming instead of forming the
+  // kernel's tail.
   int streamk;
-  long long iters;         // num_tiles * kblocks
+  int sk_tiles;            // tiles in the stream-K region (num_tiles: pure stream-K)
+  long long iters;         // sk_tiles * kblocks
   float* ws;               // [clusters][CG][128][kMmaN] fp32 partials
   unsigned* flags;         // [clusters][CG][kEpiWarps] epoch flags
   unsigned epoch;          // this launch's flag value
@@ -298,11 +304,11 @@ __device__ __forceinline__ UnitIter units_begin(const TcParams& p, int cluster, 
   UnitIter u;
   u.it = p.streamk ? sk_start(p.iters, cluster, C) : 0;
   u.end = p.streamk ? sk_start(p.iters, cluster + 1, C) : 0;
-  u.next_tile = cluster;
+  u.next_tile = (p.streamk ? p.sk_tiles : 0) + cluster;
   return u;
 }
 __device__ __forceinline__ bool units_next(const TcParams& p, int C, UnitIter& s, Unit& u) {
-  if (!p.streamk) {
+  if (!p.streamk || s.it >= s.end) {  // data-parallel tiles (after the stream-K share, if any)
     if (s.next_tile >= p.num_tiles) return false;
     u.tile = s.next_tile;
     u.kb0 = 0;
@@ -310,7 +316,6 @@ __device__ __forceinline__ bool units_next(const TcParams& p, int C, UnitIter& s
     s.next_tile += C;
     return true;
   }
-  if (s.it >= s.end) return false;
   u.tile = static_cast<int>(s.it / p.kblocks);
   u.kb0 = static_cast<int>(s.it - static_cast<long long>(u.tile) * p.kblocks);
   const long long left = s.end - s.it;
@@ -1007,13 +1012,30 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
   int clusters = p.num_tiles < max_clusters ? p.num_tiles : max_clusters;
   p.iters = static_cast<long long>(p.num_tiles) * p.kblocks;
   p.streamk = 0;
+  p.sk_tiles = 0;
   p.ws = nullptr;
   p.flags = nullptr;
   p.epoch = 0;
   void* graph_owned = nullptr;  // workspace allocated inside a CUDA graph being captured
   if (streamk) {
     clusters = max_clusters;
-    if (p.iters < 2LL * clusters) clusters = static_cast<int>(p.iters / 2 > 0 ? p.iters / 2 : 1);
+    p.sk_tiles = p.num_tiles;
+    // Hybrid: with at least one full wave of tiles, only the partial wave's tiles
+    // (mode 1) or the partial wave plus one full wave (mode 2: more stream-K work
+    // per cluster) are split; the rest run whole after each cluster's share.
+    // Measured (scripts/r02/hybrid_ab.sh, one box): C3 4096^3 0.627 ms pure
+    // stream-K -> 0.568 (mode 1) / 0.575 (mode 2); C4 50176x64x576 (18 K-blocks)
+    // 39.1 / 39.1 / 37.4 us.  Short-K tiles take mode 2, long-K mode 1;
+    // TM_SK_HYBRID=0|1|2 overrides (0: pure stream-K).
+    static const int env_hybrid = [] { const char* e = std::getenv("TM_SK_HYBRID"); return e ? std::atoi(e) : -1; }();
+    const int hybrid = env_hybrid >= 0 ? env_hybrid : (p.kblocks < 64 ? 2 : 1);
+    if (hybrid && p.num_tiles >= clusters) {
+      p.sk_tiles = p.num_tiles % clusters;
+      if (hybrid == 2 && p.num_tiles >= 2 * clusters) p.sk_tiles += clusters;
+      p.iters = static_cast<long long>(p.sk_tiles) * p.kblocks;
+    } else if (p.iters < 2LL * clusters) {
+      clusters = static_cast<int>(p.iters / 2 > 0 ? p.iters / 2 : 1);
+    }
     const size_t ws_bytes = static_cast<size_t>(clusters) * CG * kBMCta * Cfg::kMmaN * 4;
     // flags[0] of the workspace is reserved for the wave barrier counter
     const size_t flag_count = 1 + static_cast<size_t>(clusters) * CG * kEpiWarps;

@@ -191,10 +191,13 @@ def test_large_k_accuracy_sampled_rows(cfg, kind):
 
 
 @pytest.mark.parametrize("config", ["2,128,1", "2,64,1", "2,32,1", "1,128,1", "1,64,1", "1,32,1"])
-@pytest.mark.parametrize("shape", [(1060, 1060, 1060), (300, 260, 5000), (777, 1000, 3000), (129, 65, 64)])
+@pytest.mark.parametrize("shape", [(1060, 1060, 1060), (300, 260, 5000), (777, 1000, 3000), (129, 65, 64),
+                                   (2500, 2100, 700), (4100, 1000, 1200)])
 def test_streamk_fixed_order_reduction(config, shape):
     """Stream-K (tiles split across clusters, partials reduced in cluster
-    order through the workspace): parity and run-to-run bit-determinism."""
+    order through the workspace): parity and run-to-run bit-determinism.  The
+    last two shapes have more tiles than clusters, so the hybrid schedule runs
+    (the partial wave's tiles stream-K first, then whole tiles)."""
     m, n, k = shape
     pad = lambda x: (x + 3) // 4 * 4
     lda, ldb, ldc = pad(k), pad(n), pad(n)
