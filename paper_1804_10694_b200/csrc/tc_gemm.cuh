@@ -294,6 +294,7 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 // adds the later clusters' partials in cluster order).
 struct Unit {
   int tile, kb0, kb1;
+  bool dp;  // a whole data-parallel tile (the wave barrier counts these)
 };
 struct UnitIter {
   long long it, end;  // stream-K cursor
@@ -313,9 +314,11 @@ __device__ __forceinline__ bool units_next(const TcParams& p, int C, UnitIter& s
     u.tile = s.next_tile;
     u.kb0 = 0;
     u.kb1 = p.kblocks;
+    u.dp = true;
     s.next_tile += C;
     return true;
   }
+  u.dp = false;
   u.tile = static_cast<int>(s.it / p.kblocks);
   u.kb0 = static_cast<int>(s.it - static_cast<long long>(u.tile) * p.kblocks);
   const long long left = s.end - s.it;
@@ -606,14 +609,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         int wi = 0;
         int chunk_ready = -1;  // fused distributed mode: highest B chunk known to be present
         while (units_next(p, num_clusters, ui, u)) {
-          if (pi == 0 && p.wave_ctr && wi >= 1 && wi < p.full_waves) {
+          if (pi == 0 && p.wave_ctr && u.dp && wi >= 1 && wi < p.full_waves) {
             // Keep the persistent clusters in step at tile boundaries so the
             // concurrently live tiles keep sharing A/B panels in L2.
             atomicAdd(p.wave_ctr, 1u);
             const unsigned target = static_cast<unsigned>(wi) * gridDim.x;
             while (ld_acquire_gpu(p.wave_ctr) < target) __nanosleep(256);
           }
-          ++wi;
+          wi += u.dp ? 1 : 0;
           int tmi, tni;
           tile_coords(u.tile, p.tiles_m, p.tiles_n, p.group_m, tmi, tni);
           const int row0 = tmi * Cfg::kTileM + static_cast<int>(rank) * kBMCta;
@@ -1053,13 +1056,18 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
   // tiles (C4, the convolution: <= 18 K-blocks) there is little panel reuse to
   // protect and the per-tile grid-wide barrier costs 10-20%.
   static const bool wave_sync = [] { const char* e = std::getenv("TM_WAVE_SYNC"); return !(e && e[0] == '0'); }();
-  if (wave_sync && !CONV && p.kblocks >= 64 && !p.streamk && p.num_tiles / clusters >= 2) {
-    float* ws_unused = nullptr;
-    unsigned epoch_unused = 0;
-    tm_status st = streamk_workspace(stream, 0, 1, &ws_unused, &p.wave_ctr, &epoch_unused, &graph_owned);  // slot 0
-    if (st != TM_OK) return st;
-    if (!graph_owned && cudaMemsetAsync(p.wave_ctr, 0, sizeof(unsigned), stream) != cudaSuccess) return TM_ERR_CUDA;
-    p.full_waves = p.num_tiles / clusters;
+  const int dp_tiles = p.num_tiles - (p.streamk ? p.sk_tiles : 0);  // hybrid: whole waves only
+  if (wave_sync && !CONV && p.kblocks >= 64 && dp_tiles / clusters >= 2) {
+    if (p.streamk) {
+      p.wave_ctr = p.flags - 1;  // slot 0 of the stream-K flags (reserved above)
+    } else {
+      float* ws_unused = nullptr;
+      unsigned epoch_unused = 0;
+      tm_status st = streamk_workspace(stream, 0, 1, &ws_unused, &p.wave_ctr, &epoch_unused, &graph_owned);  // slot 0
+      if (st != TM_OK) return st;
+    }
+    if (cudaMemsetAsync(p.wave_ctr, 0, sizeof(unsigned), stream) != cudaSuccess) return TM_ERR_CUDA;
+    p.full_waves = dp_tiles / clusters;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CG, 1, 1);
