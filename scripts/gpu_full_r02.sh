@@ -20,7 +20,7 @@ timeout 300 python bench.py --config BLUR --steps 50 --warmup 5 2>/dev/null | ta
 cut -c1-160 gpurun_out/bench_configs_$TAG.jsonl
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference_$TAG.json 2>&1; tail -1 gpurun_out/bench_reference_$TAG.json | cut -c1-200
 TM_COOPERATIVE=0 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
-for c in C5 C4 C2; do
+for c in C5 C4 C3 C2; do
   TM_COOPERATIVE=0 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sgemm_tc -s 3 -c 1 -o gpurun_out/prof_${c}_$TAG python bench.py --config $c --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 done
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_sgemm_small -s 3 -c 1 -o gpurun_out/prof_C1_$TAG python bench.py --config C1 --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1

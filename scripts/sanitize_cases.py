@@ -32,6 +32,12 @@ for (m, n, k) in cases:
         del os.environ["TM_TC_CONFIG"]
     A, B, C = t(m, k), t(k, n), t(m, n)
     tm.sgemm_ex(A, B, C, 0.0, 0.5, 0)
+# hybrid stream-K (more tiles than clusters): partial wave split, then whole tiles
+for (m, n, k, cfg) in ((2500, 300, 200, "1,32,1"), (2500, 2100, 300, "2,64,1")):
+    os.environ["TM_TC_CONFIG"] = cfg
+    A, B, C = t(m, k), t(k, n), t(m, n)
+    tm.sgemm_ex(A, B, C, 1.5, 0.5, 1)
+    del os.environ["TM_TC_CONFIG"]
 # convolution: direct (S in {1, 3}), implicit-GEMM (forced and S = 5), SIMT; ragged rows, beta 0 / 0.5
 for (nb, h, w, c, f, r, s, pad) in [(2, 5, 140, 16, 16, 3, 3, 1), (1, 4, 130, 32, 24, 3, 3, 1),
                                      (2, 3, 131, 16, 40, 1, 1, 0), (1, 6, 37, 16, 8, 5, 5, 2),

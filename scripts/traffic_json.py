@@ -8,7 +8,7 @@ if tag == "r01":
     files = {"C5": f"ncu_c5_k_sgemm_tc_{tag}.txt", "C4": f"ncu_c4_k_sgemm_tc_{tag}.txt",
              "C3:simt": f"ncu_c3_k_sgemm_simt_{tag}.txt", "CONV": f"ncu_conv_k_conv_direct_{tag}.txt"}
 else:  # round 2 names (scripts/gpu_full_r02.sh)
-    files = {"C5": f"ncu_C5_{tag}.txt", "C4": f"ncu_C4_{tag}.txt", "C2": f"ncu_C2_{tag}.txt",
+    files = {"C5": f"ncu_C5_{tag}.txt", "C4": f"ncu_C4_{tag}.txt", "C3": f"ncu_C3_{tag}.txt", "C2": f"ncu_C2_{tag}.txt",
              "C1": f"ncu_C1_{tag}.txt", "C3:simt": f"ncu_simt_c3_{tag}.txt", "CONV": f"ncu_conv_{tag}.txt",
              "BLUR": f"ncu_blur_{tag}.txt"}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
