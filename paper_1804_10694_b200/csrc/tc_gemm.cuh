@@ -336,6 +336,24 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Spin until *p reaches a value (>= target, or == target when exact): the
+// grid-wide waits of the wave barrier and the stream-K finalizer.  All
+// clusters are co-resident (cooperative launch), so these complete unless a
+// schedule bug leaves a producer without work; then trap after ~20 s instead
+// of hanging the device.
+static __device__ __forceinline__ void spin_until(const unsigned* p, unsigned target, bool exact, unsigned sleep_ns) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    const unsigned v = ld_acquire_gpu(p);
+    if (exact ? v == target : v >= target) return;
+    __nanosleep(sleep_ns);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) __trap();
+  }
+}
+
 // Fused distributed mode: wait until B's K-chunk c has arrived (its flag,
 // written by a stream memory operation after the chunk's transfer, reaches
 // this call's epoch), then order the TMA (async-proxy) reads of that chunk
@@ -614,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // concurrently live tiles keep sharing A/B panels in L2.
             atomicAdd(p.wave_ctr, 1u);
             const unsigned target = static_cast<unsigned>(wi) * gridDim.x;
-            while (ld_acquire_gpu(p.wave_ctr) < target) __nanosleep(256);
+            spin_until(p.wave_ctr, target, false, 256);
           }
           wi += u.dp ? 1 : 0;
           int tmi, tni;
@@ -915,7 +933,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c2 = cluster_id + 1; c2 < num_clusters && sk_start(p.iters, c2, num_clusters) < tile_end; ++c2) {
           const unsigned* f = p.flags + c2 * (CG * kEpiWarps) + wslot;
           if (lane == 0) {
-            while (ld_acquire_gpu(f) != p.epoch) __nanosleep(64);
+            spin_until(f, p.epoch, true, 64);
           }
           __syncwarp();
           const unsigned seen = ld_acquire_gpu(f);  // every lane acquires (orders its own loads below)
@@ -1022,7 +1040,6 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
   void* graph_owned = nullptr;  // workspace allocated inside a CUDA graph being captured
   if (streamk) {
     clusters = max_clusters;
-    p.sk_tiles = p.num_tiles;
     // Hybrid: with at least one full wave of tiles, only the partial wave's tiles
     // (mode 1) or the partial wave plus one full wave (mode 2: more stream-K work
     // per cluster) are split; the rest run whole after each cluster's share.
@@ -1032,13 +1049,21 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
     // TM_SK_HYBRID=0|1|2 overrides (0: pure stream-K).
     static const int env_hybrid = [] { const char* e = std::getenv("TM_SK_HYBRID"); return e ? std::atoi(e) : -1; }();
     const int hybrid = env_hybrid >= 0 ? env_hybrid : (p.kblocks < 64 ? 2 : 1);
+    // Every cluster must own at least one iteration of the stream-K region (a
+    // finalizer waits for each later cluster whose range starts inside its tile,
+    // and an empty range never publishes): a hybrid region of fewer than two
+    // iterations per cluster falls back to pure stream-K, whose cluster count
+    // shrinks to half the iterations when they are that few.
+    int sk_tiles = p.num_tiles;
     if (hybrid && p.num_tiles >= clusters) {
-      p.sk_tiles = p.num_tiles % clusters;
-      if (hybrid == 2 && p.num_tiles >= 2 * clusters) p.sk_tiles += clusters;
-      p.iters = static_cast<long long>(p.sk_tiles) * p.kblocks;
-    } else if (p.iters < 2LL * clusters) {
-      clusters = static_cast<int>(p.iters / 2 > 0 ? p.iters / 2 : 1);
+      sk_tiles = p.num_tiles % clusters;
+      if (hybrid == 2 && p.num_tiles >= 2 * clusters) sk_tiles += clusters;
+      if (static_cast<long long>(sk_tiles) * p.kblocks < 2LL * clusters) sk_tiles = p.num_tiles;
     }
+    p.sk_tiles = sk_tiles;
+    p.iters = static_cast<long long>(p.sk_tiles) * p.kblocks;
+    if (p.sk_tiles == p.num_tiles && p.iters < 2LL * clusters)
+      clusters = static_cast<int>(p.iters / 2 > 0 ? p.iters / 2 : 1);
     const size_t ws_bytes = static_cast<size_t>(clusters) * CG * kBMCta * Cfg::kMmaN * 4;
     // flags[0] of the workspace is reserved for the wave barrier counter
     const size_t flag_count = 1 + static_cast<size_t>(clusters) * CG * kEpiWarps;
