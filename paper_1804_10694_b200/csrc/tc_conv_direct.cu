@@ -94,7 +94,7 @@ struct DcParams {
 
 // Role timing for TM_CONV_STATS (null stats: no cost beyond the branch).
 enum DcStat { kStMmaWaitAcc, kStMmaWaitReady, kStMmaTotal, kStSplitWaitHalo, kStSplitWaitSlot, kStSplitTotal,
-              kStEpiWaitAcc, kStEpiTotal, kStProdWaitSlot, kStProdTotal };
+              kStEpiWaitAcc, kStEpiTotal, kStProdWaitSlot, kStProdTotal, kStMmaIssue, kStMmaCommit, kStMmaLoop, kStMmaFence, kStMmaBody };
 #define DC_TIMED(slot, stmt)                                      \
   do {                                                            \
     if constexpr (ST) {                                           \
@@ -223,15 +223,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       int sl = 0, pb = 0;
       uint32_t phl = 0, pph = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const long long tb0_ = ST ? clock64() : 0;
         DC_TIMED(kStMmaWaitAcc, ptx::mbar_wait(&part_empty[pb], pph ^ 1));
         const uint32_t d = tmem_base + static_cast<uint32_t>(pb * p.n);
         uint32_t boff = 0;
         int sg = 0;  // filter stage (global over the passes)
         for (int ps = 0; ps < p.passes; ++ps) {
           DC_TIMED(kStMmaWaitReady, ptx::mbar_wait(&ready[sl], phl));
-          ptx::tc_fence_after();
+          DC_TIMED(kStMmaFence, ptx::tc_fence_after());
           uint32_t a = tmem_base + acol + static_cast<uint32_t>(sl * p.a_cols);
           const int ns = min(p.pstages, p.stages - sg);
+          const long long ti0_ = ST ? clock64() : 0;
           for (int s = 0; s < ns; ++s, ++sg) {
 #pragma unroll
             for (int ks = 0; ks < kDcBK / 8; ++ks) {
@@ -244,10 +246,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             boff += bstep;
           }
           ptx::mma_commit<1>(&a_empty[sl]);
+          if constexpr (ST) st_acc[kStMmaIssue] += static_cast<unsigned long long>(clock64() - ti0_);
           if (++sl == p.a_slots) { sl = 0; phl ^= 1; }
         }
-        ptx::mma_commit<1>(&part_full[pb]);
+        DC_TIMED(kStMmaCommit, ptx::mma_commit<1>(&part_full[pb]));
         if (++pb == p.n_part) { pb = 0; pph ^= 1; }
+        if constexpr (ST) { st_acc[kStMmaLoop] += 1; st_acc[kStMmaBody] += static_cast<unsigned long long>(clock64() - tb0_); }
       }
     }
   } else if (warp < 8) {
@@ -438,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const unsigned long long total = static_cast<unsigned long long>(clock64() - st_t0);
     unsigned long long* o = p.stats + static_cast<long long>(blockIdx.x) * 16;
     if (threadIdx.x == 0) { o[kStProdWaitSlot] = st_acc[kStProdWaitSlot]; o[kStProdTotal] = total; }
-    if (warp == 1 && lane == 0) { o[kStMmaWaitAcc] = st_acc[kStMmaWaitAcc]; o[kStMmaWaitReady] = st_acc[kStMmaWaitReady]; o[kStMmaTotal] = total; }
+    if (warp == 1 && lane == 0) { o[kStMmaWaitAcc] = st_acc[kStMmaWaitAcc]; o[kStMmaWaitReady] = st_acc[kStMmaWaitReady]; o[kStMmaTotal] = total; o[kStMmaIssue] = st_acc[kStMmaIssue]; o[kStMmaCommit] = st_acc[kStMmaCommit]; o[kStMmaLoop] = st_acc[kStMmaLoop]; o[kStMmaFence] = st_acc[kStMmaFence]; o[kStMmaBody] = st_acc[kStMmaBody]; }
     if (warp == 4 && lane == 0) { o[kStSplitWaitHalo] = st_acc[kStSplitWaitHalo]; o[kStSplitWaitSlot] = st_acc[kStSplitWaitSlot]; o[kStSplitTotal] = total; }
     if (warp == 8 && lane == 0) { o[kStEpiWaitAcc] = st_acc[kStEpiWaitAcc]; o[kStEpiTotal] = total; }
   }
@@ -516,10 +520,11 @@ int dc_plan(const ConvArgs& a, DcParams& p, int kx0, int taps) {
   (void)tiles;
   p.chunks = p.c / kDcBK;
   if (p.chunks > kDcMaxStages) return 0;
-  // Two output rows per tile when one row's MMA N is small (<= 48: the
-  // kind::tf32 floor of ~45 cycles per MMA leaves N = 96 nearly free): input
-  // rows r + 1 instead of 2r, N doubled, MMA cycles per output row -29 % at
-  // 3x3 x 16 filters; the (j, o) blocks with j - o outside [0, r) are zeros.
+  // Two output rows per tile when one row's MMA N is small (<= 48): input rows
+  // r + 1 instead of 2r, so the split reads and stores 2/3 of the rows per
+  // output at 3x3 (measured 0.433 -> 0.388 ms, scripts/r02/conv_ro.sh) while
+  // the MMAs do 4/3 the work (the (j, o) blocks with j - o outside [0, r) are
+  // zeros; kind::tf32 with A in TMEM costs N/2 cycles at any N, DESIGN 7.12).
   static const int env_ro = [] { const char* e = std::getenv("TM_CONV_RO"); return e ? std::atoi(e) : 0; }();
   p.nrow = p.fp * taps;
   p.ro = (env_ro == 1 || p.r < 2 || 2 * p.nrow > 96) ? 1 : 2;
@@ -603,9 +608,9 @@ tm_status launch_dc(const ConvArgs& a, const DcParams& p, int smem, int num_sms,
   cudaFree(q.stats);
   if (FILE* f = std::fopen(stats_path, "a")) {
     static const char* names[] = {"mma_wait_acc", "mma_wait_ready", "mma_total", "split_wait_halo", "split_wait_slot",
-                                  "split_total", "epi_wait_acc", "epi_total", "prod_wait_slot", "prod_total"};
+                                  "split_total", "epi_wait_acc", "epi_total", "prod_wait_slot", "prod_total", "mma_issue", "mma_commit", "mma_tiles", "mma_fence", "mma_body"};
     std::fprintf(f, "{\"S\": %d, \"tiles\": %d, \"grid\": %d", S, p.num_tiles, grid);
-    for (int k = 0; k < 10; ++k) {
+    for (int k = 0; k < 15; ++k) {
       double sum = 0;
       for (int b = 0; b < grid; ++b) sum += static_cast<double>(h[b * 16 + k]);
       std::fprintf(f, ", \"%s\": %.0f", names[k], sum / grid);

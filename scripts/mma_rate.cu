@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(128, 1) k_rate(int n, int a_tmem, int reps, in
       out[0] = static_cast<unsigned long long>(t1 - t0);
       out[1] = static_cast<unsigned long long>(t2 - t0);
     }
-  } else if (threadIdx.x == 32 && n_acc >= 0) {
+  } else if (warp == 1 && n_acc >= 0 && ptx::elect_one()) {  // elect: the compiler then knows one lane issues (no per-MMA R2UR waterfall)
     const uint32_t idesc = ptx::idesc_tf32(m, n, 0, 0);
     const uint64_t ad = ptx::sdesc(ptx::smem_u32(smem), 16, 1024, ptx::kLayoutSW128);
     const uint64_t bd = bsw == 64 ? ptx::sdesc(ptx::smem_u32(smem + 32 * 1024), 16, 512, ptx::kLayoutSW64)

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(192, 1) k_probe2(const __grid_constant__ CUten
   const int loads_per_panel = (p.kblocks / p.kc) * (128 / p.rows);
   int total = 0;
   for (int pn = blockIdx.x; pn < p.panels; pn += gridDim.x) total += loads_per_panel;
-  if (warp < p.issuers && lane == 0) {
+  if (warp < p.issuers && ptx::elect_one()) {  // elect: no per-load R2UR waterfall
     int g = 0, own = 0;
     uint32_t ph = 0;
     int i = 0;
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(192, 1) k_probe2(const __grid_constant__ CUten
         if (++own == p.issuers) own = 0;
         if (++g == groups) { g = 0; ph ^= 1; }
       }
-  } else if (warp == 5 && lane == 0) {
+  } else if (warp == 5 && ptx::elect_one()) {
     int g = 0;
     uint32_t ph = 0;
     for (int i = 0; i < total; ++i) {

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) k_probe(const __grid_constant__ CUtensorM
   }
   __syncthreads();
   const int pair = warp >> 1, ns = p.stages / p.pairs, s0 = pair * ns, nl = p.loads / p.pairs;
-  if ((warp & 1) == 0 && lane == 0) {
+  if ((warp & 1) == 0 && ptx::elect_one()) {  // elect: no per-load R2UR waterfall
     int s = 0; uint32_t ph = 0;
     for (int i = 0; i < nl; ++i) {
       wait_v(&empty[s0 + s], ph ^ 1, p.wait_variant);
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) k_probe(const __grid_constant__ CUtensorM
       }
       if (++s == ns) { s = 0; ph ^= 1; }
     }
-  } else if ((warp & 1) == 1 && lane == 0) {
+  } else if ((warp & 1) == 1 && ptx::elect_one()) {
     int s = 0; uint32_t ph = 0;
     for (int i = 0; i < nl; ++i) {
       wait_v(&full[s0 + s], ph, p.wait_variant);
