@@ -548,8 +548,10 @@ int dc_plan(const ConvArgs& a, DcParams& p, int kx0, int taps) {
   const int fixed = 1024 + 2 * p.bres_bytes + p.fgap + 512;
   if (fixed >= kDcMaxSmem) return 0;
   int best_rpp = 0, best_slots = 0, best_part = 0;
+  // TM_CONV_RPP (tests / experiments): cap the filter rows per pass
+  static const int env_rpp = [] { const char* e = std::getenv("TM_CONV_RPP"); return e ? std::atoi(e) : 0; }();
   for (int want_slots = 2; want_slots >= 1 && !best_rpp; --want_slots) {
-    for (int rpp = std::min(p.rin, kDcMaxStages / p.chunks); rpp >= 1; --rpp) {
+    for (int rpp = std::min({p.rin, kDcMaxStages / p.chunks, env_rpp > 0 ? env_rpp : 1 << 20}); rpp >= 1; --rpp) {
       const int a_cols = rpp * p.chunks * 2 * kDcBK;
       int part = 2, slots = (512 - 2 * p.n) / a_cols;
       if (slots < want_slots) { part = 1; slots = (512 - p.n) / a_cols; }
