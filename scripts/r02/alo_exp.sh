@@ -1,3 +1,5 @@
+# NOTE: the noalo libraries this compared were built from tc_gemm_nn.cu alone, which
+# DESIGN 7.15 shows can silently keep the product kernels -- results inconclusive, not used.
 # EXPERIMENT: A_lo staged in TMEM (tcgen05.st, the shipped rule) vs in shared memory
 # (noalo2: 2 lo stages, noalo4: 4 lo stages for stages <= 20 KiB) on C4 / C2 / C3;
 # 1xTF32 (no split) as the streaming floor of the same pipeline.  Interleaved, one box.
