@@ -185,6 +185,21 @@ def max_over_ranks(torch, dist, world, values):
     return [float(x) for x in t.tolist()]
 
 
+def soak_more(torch, dist, world, t_soak):
+    """True while the >= 1 s soak before the timed steps should go on, agreed by
+    every rank: each N > 1 step is a collective (the B broadcast / border
+    exchange), so all ranks must run the same number of steps -- a per-rank
+    wall-clock decision would leave one rank in a collective the others never
+    join."""
+    want = time.time() - t_soak < 1.0
+    if world == 1:
+        return want
+    cpu = SHARED_GPU or dist.get_backend() == "gloo"
+    t = torch.tensor([1.0 if want else 0.0], dtype=torch.float64, device="cpu" if cpu else "cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()) > 0.0
+
+
 def workload(name):
     import seeded_inputs as si
     m, n, k = si.CONFIGS[name]
@@ -418,7 +433,7 @@ def main():
         for _ in range(args.warmup):
             one()
         torch.cuda.synchronize()
-        while time.time() - t_soak < 1.0:
+        while soak_more(torch, dist, world, t_soak):
             for _ in range(8):
                 one()
             torch.cuda.synchronize()
@@ -610,8 +625,9 @@ def run_blur(args):
     if world > 1 and rank < world - 1:
         lin[rows:] = float("nan")  # received from rank + 1 every step
     lout = torch.empty((rows, M - 2, 3), dtype=torch.float32, device="cuda")
-    comm = (tm.CeComm(rank, world) if args.transport == "ce" else tm.Comm(rank, world)) if world > 1 else None
-    ce_handles = comm.exchange(B) if args.transport == "ce" and comm is not None else None
+    if world > 1 and args.transport == "ce":
+        raise SystemExit("--config BLUR: the border exchange runs over NCCL (--transport nccl)")
+    comm = tm.Comm(rank, world) if world > 1 else None
     flush = torch.ones(512 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
     flush_out = torch.empty(1, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
@@ -629,7 +645,7 @@ def run_blur(args):
             torch.sum(flush, dim=0, out=flush_out[0])
             step()
         torch.cuda.synchronize()
-        while time.time() - t_soak < 1.0:
+        while soak_more(torch, dist, world, t_soak):
             for _ in range(8):
                 torch.sum(flush, dim=0, out=flush_out[0])
                 step()

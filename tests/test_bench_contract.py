@@ -4,6 +4,7 @@ TM_BENCH_SHARED_GPU=1, copy-engine transport) print one JSON line with the
 required keys; the N = 2 line's world, transport and launch count are right."""
 import json
 import os
+import signal
 import socket
 import subprocess
 import sys
@@ -38,12 +39,21 @@ def test_bench_n2_shared_gpu_ce_transport():
     port = s.getsockname()[1]
     s.close()
     env = dict(os.environ, TM_BENCH_SHARED_GPU="1")
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
-                        "--config", "C3", "--transport", "ce", "--steps", "3", "--warmup", "3", "--no-cpu"],
-                       cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
-    assert r.returncode == 0, r.stderr[-3000:]
-    d = _last_json(r.stdout)
+    # own session: on a timeout the whole process group (torchrun and its
+    # ranks) is killed, so a hang cannot leave ranks running on the GPU
+    p = subprocess.Popen([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+                          "--config", "C3", "--transport", "ce", "--steps", "3", "--warmup", "3", "--no-cpu"],
+                         cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env,
+                         start_new_session=True)
+    try:
+        out, err = p.communicate(timeout=600)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        p.communicate()
+        raise
+    assert p.returncode == 0, err[-3000:]
+    d = _last_json(out)
     assert KEYS <= set(d)
     assert d["n_gpus"] == 2 and d["config"]["transport"] == "ce" and d["config"]["rows_per_rank"] == 2048
     assert d["gpu_launches"] == 3 * 3  # geometric chunks of K = 4096 at P = 2: 512, 1024, 2560

@@ -105,3 +105,38 @@ def test_chunk_schedule_single_process():
         assert all(k0 % 32 == 0 for k0, _ in ch)
         assert all(kb >= ka for (_, ka), (_, kb) in zip(ch, ch[1:-1]))  # non-decreasing before the last
     assert tm.dist_chunks(0, 4) == []
+
+
+def _soak_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import time
+    import torch
+    import torch.distributed as dist
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        now = time.time()
+        # rank 0's own clock says the soak is over, rank 1's says go on: both must go on
+        mixed = bench.soak_more(torch, dist, world, now - 5.0 if rank == 0 else now)
+        done = bench.soak_more(torch, dist, world, now - 5.0)  # every clock says over
+        q.put((rank, mixed, done))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_soak_decision_is_collective():
+    """bench.py's N > 1 soak loop: every step is a collective, so the decision
+    to keep soaking must be the same on every rank (a per-rank wall-clock test
+    once left one rank in a broadcast the other never joined)."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_soak_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    assert [r[1] for r in res] == [True, True] and [r[2] for r in res] == [False, False], res
