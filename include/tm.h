@@ -234,6 +234,24 @@ tm_status tm_sgemm_plan_config(int opa, int opb, int64_t m, int64_t n, int64_t k
                                int64_t lda, const float* B, int64_t ldb, float beta, const float* C, int64_t ldc,
                                int algo, int* path, int* cg, int* bn_cta, int* streamk);
 
+/* Stream-K work split of a tensor-core launch (host-only, no device): of
+ * `num_tiles` output tiles of `kblocks` K-blocks (32 k each) on `clusters`
+ * persistent clusters, *sk_tiles tiles (the first in the grouped raster) are
+ * cut into equal contiguous ranges of tile x K-block iterations, one per
+ * cluster, and reduced in cluster order; the remaining tiles run whole,
+ * data-parallel, after each cluster's share (the "hybrid" schedule;
+ * *sk_tiles == num_tiles is pure stream-K).  *clusters_used is the launch's
+ * cluster count (fewer than `clusters` only when there are fewer than two
+ * iterations per cluster).  mode: 0 pure stream-K, 1 the partial wave's
+ * tiles, 2 those plus one full wave, -1 the library default (2 when
+ * kblocks < 64, else 1).  Guarantees: every cluster owns >= 2 iterations of
+ * the region; num_tiles - *sk_tiles is a multiple of *clusters_used.  The
+ * paper's tiled loop nest (PAPER.md:753-758 tiling, 830-831 the GPU gemm)
+ * fixes the result of each tile, not this split.  TM_ERR_INVALID_VALUE on
+ * num_tiles, kblocks or clusters < 1, mode > 2, or null outputs. */
+tm_status tm_sgemm_streamk_region(int64_t num_tiles, int64_t kblocks, int clusters, int mode, int64_t* sk_tiles,
+                                  int* clusters_used);
+
 /* Name of the path tm_sgemm_ex would take for these arguments on the current
  * device ("tf32x3", "tf32x1", "simt", "simt_small", "scale", "noop", or
  * "invalid"); host-only, no launch. */

@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = [
     "tm_sgemm_plan_name", "tm_comm_get_unique_id", "tm_comm_init", "tm_comm_destroy", "tm_comm_rank",
     "tm_dist_rows", "tm_dist_chunk", "tm_sgemm_dist", "tm_sgemm_dist_fused", "tm_sgemm_dist_loopback", "tm_sgemm_dist_allgather", "tm_comm_check", "tm_comm_bytes_received",
     "tm_sgemm_tune", "tm_tune_cache_size", "tm_tune_cache_clear", "tm_tune_cache_save", "tm_tune_cache_load",
-    "tm_sgemm_plan_config", "tm_blur", "tm_blur_dist", "tm_blur_dist_loopback",
+    "tm_sgemm_plan_config", "tm_sgemm_streamk_region", "tm_blur", "tm_blur_dist", "tm_blur_dist_loopback",
     "tm_sgemm_summa", "tm_summa_panel", "tm_sgemm_summa_loopback", "tm_conv2d_plan_name",
     "tm_ipc_export", "tm_ce_create", "tm_ce_connect", "tm_ce_destroy", "tm_ce_bytes_received", "tm_sgemm_dist_ce",
 ]
@@ -63,6 +63,7 @@ def _load():
     L.tm_status_string.argtypes = [ci]
     L.tm_status_string.restype = ctypes.c_char_p
     L.tm_dist_rows.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.tm_sgemm_streamk_region.argtypes = [i64, i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(ci)]
     L.tm_dist_chunk.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.tm_comm_get_unique_id.argtypes = [vp]
     L.tm_comm_init.argtypes = [ctypes.POINTER(vp), ci, ci, vp]
@@ -361,6 +362,14 @@ def sgemm_host(A, B, C, alpha: float = 1.0, beta: float = 0.0, algo: int = ALGO_
                            ldc, _stream(stream), int(algo))
     _check(st, "tm_sgemm_host")
     return C
+
+
+def streamk_region(num_tiles: int, kblocks: int, clusters: int, mode: int = -1):
+    """(sk_tiles, clusters_used) of a stream-K launch (tm_sgemm_streamk_region)."""
+    sk, cu = ctypes.c_int64(), ctypes.c_int()
+    _check(lib.tm_sgemm_streamk_region(num_tiles, kblocks, clusters, mode, ctypes.byref(sk), ctypes.byref(cu)),
+           "tm_sgemm_streamk_region")
+    return int(sk.value), int(cu.value)
 
 
 def dist_rows(m: int, nranks: int, rank: int):

@@ -40,6 +40,29 @@ bool plan_streamk(int64_t m, int64_t n, int64_t k, int cg, int bn_cta, int num_s
   return tiles * kb >= 2 * units;
 }
 
+// Stream-K region of a stream-K launch (tc_gemm.cuh launch_kernel; DESIGN 6.1
+// "hybrid stream-K"): how many of the tiles are split over the clusters (the
+// first sk_tiles of the raster; the rest run whole after each cluster's share)
+// and how many clusters the launch uses.  mode: 0 pure stream-K, 1 the partial
+// wave, 2 the partial wave plus one full wave, < 0 the default (2 for tiles of
+// fewer than 64 K-blocks, else 1).  Invariants (tests/test_abi.py): every
+// cluster owns at least two iterations of the region -- a finalizer waits for
+// each later cluster whose range starts inside its tile, and an empty range
+// would never publish -- and the tiles after the region form whole waves.
+int64_t streamk_region(int64_t num_tiles, int64_t kblocks, int clusters, int mode, int* clusters_used) {
+  if (mode < 0) mode = kblocks < 64 ? 2 : 1;
+  int64_t sk = num_tiles;
+  if (mode && num_tiles >= clusters) {
+    sk = num_tiles % clusters;
+    if (mode == 2 && num_tiles >= 2LL * clusters) sk += clusters;
+    if (sk * kblocks < 2LL * clusters) sk = num_tiles;  // too few iterations: pure stream-K
+  }
+  const int64_t iters = sk * kblocks;
+  if (sk == num_tiles && iters < 2LL * clusters) clusters = static_cast<int>(iters / 2 > 0 ? iters / 2 : 1);
+  *clusters_used = clusters;
+  return sk;
+}
+
 TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms) {
   static const TcChoice cands[] = {{2, 128, 1, false}, {2, 64, 1, false}, {2, 32, 1, false},
                                    {1, 128, 1, false}, {1, 64, 1, false}, {1, 32, 1, false}};
@@ -87,3 +110,11 @@ TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms) {
 }
 
 }  // namespace tmk
+
+extern "C" tm_status tm_sgemm_streamk_region(int64_t num_tiles, int64_t kblocks, int clusters, int mode,
+                                             int64_t* sk_tiles, int* clusters_used) {
+  if (num_tiles < 1 || kblocks < 1 || clusters < 1 || mode > 2 || !sk_tiles || !clusters_used)
+    return TM_ERR_INVALID_VALUE;
+  *sk_tiles = tmk::streamk_region(num_tiles, kblocks, clusters, mode, clusters_used);
+  return TM_OK;
+}

@@ -1048,22 +1048,10 @@ tm_status launch_kernel(const CUtensorMap& tmA, const CUtensorMap& tmB, TcParams
     // 39.1 / 39.1 / 37.4 us.  Short-K tiles take mode 2, long-K mode 1;
     // TM_SK_HYBRID=0|1|2 overrides (0: pure stream-K).
     static const int env_hybrid = [] { const char* e = std::getenv("TM_SK_HYBRID"); return e ? std::atoi(e) : -1; }();
-    const int hybrid = env_hybrid >= 0 ? env_hybrid : (p.kblocks < 64 ? 2 : 1);
-    // Every cluster must own at least one iteration of the stream-K region (a
-    // finalizer waits for each later cluster whose range starts inside its tile,
-    // and an empty range never publishes): a hybrid region of fewer than two
-    // iterations per cluster falls back to pure stream-K, whose cluster count
-    // shrinks to half the iterations when they are that few.
-    int sk_tiles = p.num_tiles;
-    if (hybrid && p.num_tiles >= clusters) {
-      sk_tiles = p.num_tiles % clusters;
-      if (hybrid == 2 && p.num_tiles >= 2 * clusters) sk_tiles += clusters;
-      if (static_cast<long long>(sk_tiles) * p.kblocks < 2LL * clusters) sk_tiles = p.num_tiles;
-    }
-    p.sk_tiles = sk_tiles;
+    // The region and the cluster count (plan.cpp streamk_region): every cluster
+    // owns >= 2 iterations of the region, the remaining tiles form whole waves.
+    p.sk_tiles = static_cast<int>(streamk_region(p.num_tiles, p.kblocks, clusters, env_hybrid, &clusters));
     p.iters = static_cast<long long>(p.sk_tiles) * p.kblocks;
-    if (p.sk_tiles == p.num_tiles && p.iters < 2LL * clusters)
-      clusters = static_cast<int>(p.iters / 2 > 0 ? p.iters / 2 : 1);
     const size_t ws_bytes = static_cast<size_t>(clusters) * CG * kBMCta * Cfg::kMmaN * 4;
     // flags[0] of the workspace is reserved for the wave barrier counter
     const size_t flag_count = 1 + static_cast<size_t>(clusters) * CG * kEpiWarps;

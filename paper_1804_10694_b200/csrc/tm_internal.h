@@ -142,5 +142,6 @@ tm_status launch_blur(int64_t i0, int64_t i1, int64_t M, const float* in, int64_
 TcChoice plan_tc(int64_t m, int64_t n, int64_t k, int num_sms);
 // Whether a configuration should run stream-K for this shape.
 bool plan_streamk(int64_t m, int64_t n, int64_t k, int cg, int bn_cta, int num_sms);
+int64_t streamk_region(int64_t num_tiles, int64_t kblocks, int clusters, int mode, int* clusters_used);
 
 }  // namespace tmk

@@ -205,3 +205,39 @@ def test_conv_plan_names_for_the_paper_filter_sizes():
     assert tm.conv2d_plan_name(1, 8, 8, 18, 16, 3, 3, 1) == "simt"
     assert tm.conv2d_plan_name(1, 8, 8, 16, 16, 3, 3, 1, alpha=0.0) == "scale"
     assert tm.conv2d_plan_name(1, 2, 2, 16, 16, 3, 3, 0) == "invalid"  # no output pixel
+
+
+def _sk_ranges(iters, clusters):
+    return [(iters * c // clusters, iters * (c + 1) // clusters) for c in range(clusters)]
+
+
+def test_streamk_region_invariants():
+    """Host-only stream-K split (tm_sgemm_streamk_region, the rule the kernel
+    launch uses): every cluster owns at least two iterations of the region (an
+    empty range would never publish the partial its tile's finalizer waits
+    for), the tiles after the region form whole waves, and the modes select
+    what DESIGN 6.1 says."""
+
+    for clusters in (1, 2, 37, 74, 148):
+        for tiles in (1, 2, 3, 36, 45, 73, 74, 75, 80, 100, 147, 148, 149, 196, 256, 300, 1025):
+            for kb in (1, 2, 3, 18, 34, 63, 64, 128, 512):
+                for mode in (-1, 0, 1, 2):
+                    sk, cu = tm.streamk_region(tiles, kb, clusters, mode)
+                    assert 0 <= sk <= tiles and 1 <= cu <= clusters, (tiles, kb, clusters, mode, sk, cu)
+                    assert (tiles - sk) % cu == 0, (tiles, kb, clusters, mode, sk, cu)
+                    iters = sk * kb
+                    if sk < tiles:  # hybrid: every cluster keeps its full count
+                        assert cu == clusters and iters >= 2 * cu
+                    if iters >= 2:
+                        assert all(e - b >= 2 for b, e in _sk_ranges(iters, cu)), (tiles, kb, clusters, mode, sk, cu)
+                    if mode == 0:
+                        assert sk == tiles
+    # the cases of DESIGN 6.1: C3 (256 tiles of 128 K-blocks on 74 clusters) splits its
+    # partial wave; C4 (196 of 18) the partial wave plus one wave; 80 tiles of 2
+    # K-blocks (12 iterations for 74 clusters) falls back to pure stream-K on 80 clusters
+    assert tm.streamk_region(256, 128, 74) == (34, 74)
+    assert tm.streamk_region(196, 18, 74) == (48 + 74, 74)
+    assert tm.streamk_region(80, 2, 74) == (80, 74)
+    assert tm.streamk_region(30, 1, 74) == (30, 15)
+    with pytest.raises(tm.TmError):
+        tm.streamk_region(0, 1, 74)
