@@ -249,10 +249,11 @@ def tune(A, B, C, alpha: float = 1.0, beta: float = 0.0, opa: str = "N", opb: st
     return cg.value, bn.value, sk.value, ms.value
 
 
-def plan_config(m, n, k, alpha=1.0, beta=0.0, A_ptr=1 << 12, lda=None, B_ptr=1 << 16, ldb=None, C_ptr=1 << 24,
+def plan_config(m, n, k, alpha=1.0, beta=0.0, A_ptr=1 << 40, lda=None, B_ptr=2 << 40, ldb=None, C_ptr=3 << 40,
                 ldc=None, opa="N", opb="N", algo=ALGO_AUTO):
     """Host-only: (path, cg, bn_cta, streamk) tm_sgemm_op would use; path 3 =
-    tensor cores, 4 = SIMT, 2 = scale, 1 = no-op, 0 = invalid."""
+    tensor cores, 4 = SIMT, 2 = scale, 1 = no-op, 0 = invalid.  The default
+    pointers are 1 TiB apart, so no operand overlaps C at any size."""
     ta, tb = opa == "T", opb == "T"
     lda = (max(m, 1) if ta else max(k, 1)) if lda is None else lda
     ldb = (max(k, 1) if tb else max(n, 1)) if ldb is None else ldb

@@ -241,3 +241,15 @@ def test_streamk_region_invariants():
     assert tm.streamk_region(30, 1, 74) == (30, 15)
     with pytest.raises(tm.TmError):
         tm.streamk_region(0, 1, 74)
+
+
+def test_plan_config_large_shapes():
+    """Host-only planner at BASELINE.json's sizes: the tensor-core path, the
+    cluster tile and the schedule DESIGN 6.1 / BASELINE.md report (stream-K for
+    the partial-wave shapes C2/C3/C4, data-parallel for C3b/C5)."""
+    TC = 3
+    assert tm.plan_config(16384, 16384, 16384, 1.5, 0.5) == (TC, 2, 128, 0)
+    assert tm.plan_config(8192, 8192, 8192, 1.5, 0.5) == (TC, 2, 128, 0)
+    assert tm.plan_config(4096, 4096, 4096, 1.5, 0.5) == (TC, 2, 128, 1)
+    assert tm.plan_config(50176, 64, 576, 1.5, 0.5) == (TC, 2, 32, 1)
+    assert tm.plan_config(1060, 1060, 1060, 1.5, 0.5) == (TC, 2, 64, 1)
