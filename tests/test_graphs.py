@@ -50,7 +50,7 @@ def test_captured_sgemm_replays(cfg):
         assert err <= TOL, (cfg, rep, err)
 
 
-@pytest.mark.parametrize("cfg", ["2,64,1", "2,128,0"])
+@pytest.mark.parametrize("cfg", ["2,64,1", "2,128,0", "2,128,1"])
 def test_default_graph_idiom_and_replay_on_other_streams(cfg):
     """The standard torch.cuda.graph idiom (warm-up on a side stream, capture on
     torch's own capture stream, no stream argument): stream-K and wave-barrier
@@ -59,7 +59,9 @@ def test_default_graph_idiom_and_replay_on_other_streams(cfg):
     of the same shape, and direct calls in between do not share flags."""
     import torch
     import paper_1804_10694_b200 as tm
-    # 2,128,0 at 4096 x 4096 x 2048: 256 tiles on 74 clusters, 64 K-blocks -> wave barrier
+    # 2,128,0 at 4096 x 4096 x 2048: 256 tiles on 74 clusters, 64 K-blocks -> wave barrier;
+    # 2,128,1 there: hybrid stream-K (34 tiles split) + the barrier over its 3 whole waves,
+    # whose counter is slot 0 of the graph-owned stream-K flags
     m, n, k = (1060, 1060, 1060) if cfg == "2,64,1" else (4096, 4096, 2048)
     A, B, _ = si.matrices(m, n, k, 43)
     dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
