@@ -98,3 +98,34 @@ def test_colmajor_blas_entry(ta, tb):
     torch.cuda.synchronize()
     Cgpu = dC.cpu().numpy().T  # back to the m x n mathematical matrix
     assert float(np.max(oracle.normalized_error(Cgpu, R, D))) <= TOL
+
+
+@pytest.mark.parametrize("opa,opb", [("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")])
+@pytest.mark.parametrize("algo,tol", [(1, 1e-5), (4, 1e-5), (3, 2.0 ** -9 + 2.0 ** -14)])
+def test_op_hybrid_streamk_every_precision(opa, opb, algo, tol):
+    """The hybrid stream-K schedule (partial wave + one wave split, then whole
+    tiles: 170 tiles of 256 x 128 on 74 clusters, 22 K-blocks) under every
+    operand layout and precision variant (3xTF32, BF16x9 at 1e-5; 1xTF32 at its
+    own bound, include/tm.h), against the oracle on sampled rows."""
+    import os
+    import torch
+    import paper_1804_10694_b200 as tm
+    m, n, k = 2500, 2100, 700
+    g = si.rng(11 + algo)
+    A = _stored(g, *((k, m) if opa == "T" else (m, k)), _pad(m if opa == "T" else k))
+    B = _stored(g, *((n, k) if opb == "T" else (k, n)), _pad(k if opb == "T" else n))
+    C0 = _stored(g, m, n, _pad(n))
+    os.environ["TM_TC_CONFIG"] = "2,64,1"
+    try:
+        dA, dB, dC = _dev(A), _dev(B), _dev(C0)
+        tm.sgemm_op(dA, dB, dC, si.ALPHA, si.BETA, opa, opb, algo=algo)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["TM_TC_CONFIG"]
+    assert tm.streamk_region(10 * 17, 22, 74) == (22 + 74, 74)
+    rows = si.sample_rows(m, count=96)
+    Ar = A[rows] if opa == "N" else A[:, rows]
+    R, D = oracle.sgemm(si.ALPHA, np.ascontiguousarray(Ar), np.ascontiguousarray(B), si.BETA,
+                        np.ascontiguousarray(C0[rows]), opa=opa, opb=opb)
+    err = float(np.max(oracle.normalized_error(dC.cpu().numpy()[rows], R, D)))
+    assert err <= tol, (opa, opb, algo, err)
